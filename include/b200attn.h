@@ -1,0 +1,139 @@
+/*
+ * b200attn.h — C ABI of the B200-native flash-attention forward (prefill + paged decode).
+ *
+ * This is the drop-in boundary for the single line of the reference runner that launches a
+ * kernel for one (config, shape):
+ *     ref/pkg/runner/src/ktune_triton_runner/backends.py:164-165   self.kernel[grid](*args, **kwargs)
+ * where `kwargs` are the space parameters mapped by KernelBinding.kernel_kwargs
+ * (ref/pkg/runner/src/ktune_triton_runner/binding.py:146-147) and the space is
+ * ref/pkg/src/ktune/fixtures/flash_attention.space.json:3-16.  The variant structs below carry
+ * exactly those knobs; the params structs carry borrowed device pointers and sizes.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers owned by the caller (borrowed for the call). No
+ *     allocation happens inside any entry point; split-KV scratch is caller-provided
+ *     (size it with b200attn_decode_workspace_size).
+ *   - `stream` is a cudaStream_t passed as void*. Launches are stream-ordered and reentrant.
+ *   - Return codes map onto the ktune protocol statuses (ref/pkg/runner/src/ktune_triton_runner/
+ *     backends.py:200-205, server.py:85-99): UNSUPPORTED_CONFIG / SMEM / TMEM -> "invalid",
+ *     BAD_ARGS / CUDA_ERROR -> "error".  b200attn_last_error() holds the message.
+ *   - Tensors are bf16 and contiguous: q/k/v/o [tokens, heads, 128]; paged caches
+ *     [num_blocks, block_size, kv_heads, 128] (the vLLM paged layout the paper's kernel
+ *     family uses).
+ */
+#ifndef B200ATTN_H_
+#define B200ATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B200ATTN_ABI_VERSION 1
+
+typedef enum {
+  B200ATTN_OK = 0,
+  B200ATTN_UNSUPPORTED_CONFIG = 1, /* config has no compiled sm_100a variant      -> invalid */
+  B200ATTN_SMEM_OVERFLOW = 2,      /* variant needs > 227 KB shared memory         -> invalid */
+  B200ATTN_TMEM_OVERFLOW = 3,      /* variant needs > 512 TMEM columns             -> invalid */
+  B200ATTN_BAD_ARGS = 4,           /* shapes / pointers inconsistent               -> error   */
+  B200ATTN_CUDA_ERROR = 5          /* launch or device error (see last_error)      -> error   */
+} b200attn_status;
+
+/* One point of flash_attention.space.json (ref/pkg/src/ktune/fixtures/flash_attention.space.json:3-16). */
+typedef struct {
+  int32_t block_m;      /* BLOCK_M: query rows per CTA summed over its q heads: 128 (1 tile) | 256 (head pair) */
+  int32_t block_n;      /* BLOCK_N: KV rows per pipeline step: 64 | 128                                         */
+  int32_t num_warps;    /* softmax warps per 128-row Q tile: 4 (one thread per TMEM lane)                        */
+  int32_t num_stages;   /* depth of the K/V TMA ring (32-KB / 16-KB slots)                                       */
+  int32_t waves_per_eu; /* AMD occupancy hint; only 1 is meaningful on sm_100a                                   */
+  int32_t pre_load_v;   /* V_j is always issued right behind K_j on the shared ring; accepted for parity         */
+} b200attn_prefill_variant;
+
+typedef struct {
+  const void* q;              /* [total_tokens, num_q_heads, head_dim] bf16  */
+  const void* k;              /* [total_tokens, num_kv_heads, head_dim] bf16 */
+  const void* v;              /* [total_tokens, num_kv_heads, head_dim] bf16 */
+  void* o;                    /* [total_tokens, num_q_heads, head_dim] bf16  */
+  const int32_t* cu_seqlens;  /* [num_seqs + 1], device                      */
+  float* lse;                 /* optional [num_q_heads, total_tokens] fp32 natural-log LSE, may be NULL */
+  int32_t num_seqs;
+  int32_t total_tokens;
+  int32_t max_seqlen;
+  int32_t num_q_heads;
+  int32_t num_kv_heads;
+  int32_t head_dim;           /* 128 */
+  int32_t causal;             /* 1: key j attends iff j <= query position (q_len == k_len) */
+  float softmax_scale;        /* <= 0 -> 1/sqrt(head_dim) */
+} b200attn_prefill_params;
+
+/* One point of spaces/paged_decode.space.json. */
+typedef struct {
+  int32_t num_splits; /* split-KV factor; 0 = heuristic (fill 148 SMs)                        */
+  int32_t num_stages; /* depth of the K/V page-gather ring (32-KB slots)                      */
+  int32_t tile_n;     /* tokens per MMA tile: 128                                             */
+} b200attn_decode_variant;
+
+typedef struct {
+  const void* q;              /* [batch, num_q_heads, head_dim] bf16                 */
+  const void* k_cache;        /* [num_blocks, block_size, num_kv_heads, head_dim] bf16 */
+  const void* v_cache;        /* same                                                */
+  const int32_t* block_table; /* [batch, max_blocks_per_seq]                         */
+  const int32_t* seq_lens;    /* [batch] cached tokens incl. the current one         */
+  void* o;                    /* [batch, num_q_heads, head_dim] bf16                 */
+  void* workspace;            /* split partials; b200attn_decode_workspace_size bytes */
+  size_t workspace_bytes;
+  int32_t batch;
+  int32_t num_q_heads;
+  int32_t num_kv_heads;
+  int32_t head_dim;           /* 128 */
+  int32_t block_size;         /* tokens per page: 8..128, power of two */
+  int32_t num_blocks;
+  int32_t max_blocks_per_seq;
+  int32_t max_seq_len;        /* upper bound of seq_lens (sizes the split grid) */
+  float softmax_scale;
+} b200attn_decode_params;
+
+int b200attn_abi_version(void);
+const char* b200attn_build_info(void);
+const char* b200attn_status_string(int status);
+const char* b200attn_last_error(void);
+
+/* Validity of a config for a shape without launching; fills `reason` for non-OK codes. */
+int b200attn_prefill_supported(const b200attn_prefill_params* p, const b200attn_prefill_variant* v,
+                               char* reason, size_t reason_len);
+int b200attn_decode_supported(const b200attn_decode_params* p, const b200attn_decode_variant* v,
+                              char* reason, size_t reason_len);
+
+/* K1: causal (or full) varlen prefill. */
+int b200attn_prefill(const b200attn_prefill_params* p, const b200attn_prefill_variant* v, void* stream);
+
+/* K2 (+K3): paged split-KV decode; the combine runs iff the resolved num_splits > 1. */
+size_t b200attn_decode_workspace_size(const b200attn_decode_params* p, const b200attn_decode_variant* v);
+int b200attn_decode_num_splits(const b200attn_decode_params* p, const b200attn_decode_variant* v);
+int b200attn_decode(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream);
+
+/* K3 alone: O[rows,128] = combine of part_o [rows, splits, 128] fp32 and part_ml [rows, splits, 2]
+ * (running max in log2 units, running sum). */
+int b200attn_combine(const float* part_o, const float* part_ml, void* o, int32_t rows, int32_t num_splits,
+                     void* stream);
+
+/* Paged KV-cache append: write new_k/new_v [num_tokens, kv_heads, 128] into the
+ * pages named by slot_mapping[num_tokens] (slot = page * block_size + offset; < 0 skips the token). */
+int b200attn_cache_append(const void* new_k, const void* new_v, void* k_cache, void* v_cache,
+                          const int64_t* slot_mapping, int32_t num_tokens, int32_t num_kv_heads,
+                          int32_t head_dim, int32_t block_size, int32_t num_blocks, void* stream);
+
+/* Descriptor self-test of the tcgen05 path (one CTA, no TMA):
+ *   mode 0: D[128x128]  = A[128x128] . B[128x128]^T   A, B K-major
+ *   mode 1: D[128x128]  = A[128x128] . B[128x128]     B MN-major ([K][N] row-major)
+ *   mode 2: D[128x16]   = A^T . B^T   with A [128(K)][128(M)] MN-major, B [16][128] K-major
+ * A, B bf16 device pointers; D fp32 device pointer. */
+int b200attn_selftest_umma(int mode, const void* a, const void* b, float* d, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200ATTN_H_ */

@@ -1,0 +1,223 @@
+"""Public attention entry points: ``prefill_varlen``, ``paged_decode``, ``cache_append``.
+
+These are the framework's drop-in for the kernel call the reference runner makes for one
+(config, shape) — ``self.kernel[grid](*args, **kwargs)`` (ref/pkg/runner/src/ktune_triton_runner/
+backends.py:164-165) — with ``config`` keyed by the autotuner space's parameter names exactly as
+``KernelBinding.kernel_kwargs`` produces them (ref/pkg/runner/src/ktune_triton_runner/binding.py:146-147;
+space: ref/pkg/src/ktune/fixtures/flash_attention.space.json:3-16).  Layouts follow the paper's
+kernel family as upstreamed in vLLM: q/k/v ``[tokens, heads, 128]``, paged caches
+``[num_blocks, block_size, kv_heads, 128]``.
+
+Every call goes to libb200attn.so (sm_100a tcgen05/TMA kernels).  torch is used only for device
+memory and the current CUDA stream.
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Mapping, Optional
+
+import torch
+
+from . import _native
+from .dispatch import default_decode_config, default_prefill_config
+
+PREFILL_PARAMS = ("BLOCK_M", "BLOCK_N", "num_warps", "num_stages", "waves_per_eu", "PRE_LOAD_V")
+DECODE_PARAMS = ("num_splits", "num_stages", "TILE_N")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()
+
+
+def _check(t: torch.Tensor, name: str, dtype=torch.bfloat16, ndim=None):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path exists)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if ndim is not None and t.dim() != ndim:
+        raise ValueError(f"{name} must be {ndim}-D, got shape {tuple(t.shape)}")
+
+
+def prefill_variant(config: Mapping) -> _native.PrefillVariant:
+    missing = [p for p in PREFILL_PARAMS if p not in config]
+    if missing:
+        raise KeyError(f"config is missing space parameter {missing[0]!r}")
+    return _native.PrefillVariant(int(config["BLOCK_M"]), int(config["BLOCK_N"]), int(config["num_warps"]),
+                                  int(config["num_stages"]), int(config["waves_per_eu"]),
+                                  int(bool(config["PRE_LOAD_V"])))
+
+
+def decode_variant(config: Mapping) -> _native.DecodeVariant:
+    missing = [p for p in DECODE_PARAMS if p not in config]
+    if missing:
+        raise KeyError(f"config is missing space parameter {missing[0]!r}")
+    return _native.DecodeVariant(int(config["num_splits"]), int(config["num_stages"]), int(config["TILE_N"]))
+
+
+def _prefill_params(q, k, v, out, cu_seqlens, max_seqlen, softmax_scale, causal, lse):
+    T, Hq, D = q.shape
+    return _native.PrefillParams(
+        _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(cu_seqlens), _ptr(lse), cu_seqlens.numel() - 1, T,
+        int(max_seqlen), Hq, k.shape[1], D, int(bool(causal)), float(softmax_scale or 0.0))
+
+
+def prefill_supported(q_shape, kv_heads, num_seqs, max_seqlen, config: Mapping, causal=True):
+    """(ok, reason) for a config on a shape, without launching."""
+    lib = _native.load()
+    T, Hq, D = q_shape
+    p = _native.PrefillParams(None, None, None, None, None, None, num_seqs, T, max_seqlen, Hq, kv_heads, D,
+                              int(causal), 0.0)
+    buf = _native.reason_buffer()
+    rc = lib.b200attn_prefill_supported(p, prefill_variant(config), buf, len(buf))
+    return rc, buf.value.decode()
+
+
+def prefill_varlen(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, cu_seqlens: torch.Tensor, max_seqlen: int,
+                   out: Optional[torch.Tensor] = None, softmax_scale: Optional[float] = None, causal: bool = True,
+                   config: Optional[Mapping] = None, return_lse: bool = False):
+    """Causal varlen prefill: q [T,Hq,128], k/v [T,Hkv,128] bf16, cu_seqlens [B+1] int32 (device).
+
+    ``config`` is a flash_attention.space.json point (BLOCK_M, BLOCK_N, num_warps, num_stages,
+    waves_per_eu, PRE_LOAD_V); default: the per-shape dispatch table.
+    """
+    lib = _native.load()
+    for t, n in ((q, "q"), (k, "k"), (v, "v")):
+        _check(t, n, ndim=3)
+    _check(cu_seqlens, "cu_seqlens", dtype=torch.int32, ndim=1)
+    if k.shape != v.shape or k.shape[0] != q.shape[0] or k.shape[2] != q.shape[2]:
+        raise ValueError(f"shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
+    if out is None:
+        out = torch.empty_like(q)
+    else:
+        _check(out, "out", ndim=3)
+    lse = torch.empty(q.shape[1], q.shape[0], device=q.device, dtype=torch.float32) if return_lse else None
+    if config is None:
+        config = default_prefill_config(num_seqs=cu_seqlens.numel() - 1, total_tokens=q.shape[0],
+                                        max_seqlen=int(max_seqlen), num_q_heads=q.shape[1],
+                                        num_kv_heads=k.shape[1], head_dim=q.shape[2], causal=causal)
+    p = _prefill_params(q, k, v, out, cu_seqlens, max_seqlen, softmax_scale, causal, lse)
+    _native.check(lib.b200attn_prefill(p, prefill_variant(config), torch.cuda.current_stream(q.device).cuda_stream))
+    return (out, lse) if return_lse else out
+
+
+_workspaces: dict = {}
+
+
+def _workspace(device, nbytes: int) -> Optional[torch.Tensor]:
+    if nbytes == 0:
+        return None
+    key = (device.type, device.index)
+    buf = _workspaces.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _workspaces[key] = buf
+    return buf
+
+
+def _decode_params(q, k_cache, v_cache, block_table, seq_lens, out, max_seq_len, softmax_scale, ws=None, ws_bytes=0):
+    B, Hq, D = q.shape
+    NB, bs, Hkv, _ = k_cache.shape
+    return _native.DecodeParams(
+        _ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(block_table), _ptr(seq_lens), _ptr(out), _ptr(ws), ws_bytes, B,
+        Hq, Hkv, D, bs, NB, block_table.shape[1], int(max_seq_len), float(softmax_scale or 0.0))
+
+
+def decode_supported(q_shape, cache_shape, max_blocks_per_seq, max_seq_len, config: Mapping):
+    lib = _native.load()
+    B, Hq, D = q_shape
+    NB, bs, Hkv, _ = cache_shape
+    p = _native.DecodeParams(None, None, None, None, None, None, None, 0, B, Hq, Hkv, D, bs, NB, max_blocks_per_seq,
+                             max_seq_len, 0.0)
+    buf = _native.reason_buffer()
+    rc = lib.b200attn_decode_supported(p, decode_variant(config), buf, len(buf))
+    return rc, buf.value.decode()
+
+
+def paged_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, block_table: torch.Tensor,
+                 seq_lens: torch.Tensor, max_seq_len: Optional[int] = None, out: Optional[torch.Tensor] = None,
+                 softmax_scale: Optional[float] = None, config: Optional[Mapping] = None):
+    """Paged-KV decode: q [B,Hq,128]; caches [NB,bs,Hkv,128] bf16; block_table [B,maxblk] int32;
+    seq_lens [B] int32.  ``max_seq_len`` (host int) sizes the split grid; defaults to the
+    block-table capacity so no device->host sync is needed.
+    """
+    lib = _native.load()
+    _check(q, "q", ndim=3)
+    _check(k_cache, "k_cache", ndim=4)
+    _check(v_cache, "v_cache", ndim=4)
+    _check(block_table, "block_table", dtype=torch.int32, ndim=2)
+    _check(seq_lens, "seq_lens", dtype=torch.int32, ndim=1)
+    if k_cache.shape != v_cache.shape:
+        raise ValueError("k_cache / v_cache shape mismatch")
+    if max_seq_len is None:
+        max_seq_len = block_table.shape[1] * k_cache.shape[1]
+    if out is None:
+        out = torch.empty_like(q)
+    else:
+        _check(out, "out", ndim=3)
+    if config is None:
+        config = default_decode_config(batch_size=q.shape[0], seq_len=int(max_seq_len), num_q_heads=q.shape[1],
+                                       num_kv_heads=k_cache.shape[2], head_dim=q.shape[2],
+                                       block_size=k_cache.shape[1])
+    var = decode_variant(config)
+    p = _decode_params(q, k_cache, v_cache, block_table, seq_lens, out, max_seq_len, softmax_scale)
+    nbytes = lib.b200attn_decode_workspace_size(p, var)
+    ws = _workspace(q.device, nbytes)
+    if ws is not None:
+        p.workspace = ws.data_ptr()
+        p.workspace_bytes = ws.numel()
+    _native.check(lib.b200attn_decode(p, var, torch.cuda.current_stream(q.device).cuda_stream))
+    return out
+
+
+def decode_num_splits(q_shape, cache_shape, max_blocks_per_seq, max_seq_len, config: Mapping) -> int:
+    lib = _native.load()
+    B, Hq, D = q_shape
+    NB, bs, Hkv, _ = cache_shape
+    p = _native.DecodeParams(None, None, None, None, None, None, None, 0, B, Hq, Hkv, D, bs, NB, max_blocks_per_seq,
+                             max_seq_len, 0.0)
+    return int(lib.b200attn_decode_num_splits(p, decode_variant(config)))
+
+
+def combine(part_o: torch.Tensor, part_ml: torch.Tensor, out: torch.Tensor):
+    """K3 alone: part_o [rows, S, 128] fp32, part_ml [rows, S, 2] (max in log2 units, sum) -> out [rows,128]."""
+    lib = _native.load()
+    _check(part_o, "part_o", dtype=torch.float32, ndim=3)
+    _check(part_ml, "part_ml", dtype=torch.float32, ndim=3)
+    _check(out, "out")
+    rows, S, _ = part_o.shape
+    _native.check(lib.b200attn_combine(_ptr(part_o), _ptr(part_ml), _ptr(out), rows, S,
+                                       torch.cuda.current_stream(out.device).cuda_stream))
+    return out
+
+
+def cache_append(new_k: torch.Tensor, new_v: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
+                 slot_mapping: torch.Tensor):
+    """Write new_k/new_v [N, Hkv, 128] into pages: slot = page * block_size + offset (int64, < 0 skips)."""
+    lib = _native.load()
+    _check(new_k, "new_k", ndim=3)
+    _check(new_v, "new_v", ndim=3)
+    _check(k_cache, "k_cache", ndim=4)
+    _check(v_cache, "v_cache", ndim=4)
+    _check(slot_mapping, "slot_mapping", dtype=torch.int64, ndim=1)
+    NB, bs, Hkv, D = k_cache.shape
+    _native.check(lib.b200attn_cache_append(_ptr(new_k), _ptr(new_v), _ptr(k_cache), _ptr(v_cache),
+                                            _ptr(slot_mapping), new_k.shape[0], Hkv, D, bs, NB,
+                                            torch.cuda.current_stream(new_k.device).cuda_stream))
+
+
+def selftest_umma(mode: int, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """tcgen05 descriptor self-test (see include/b200attn.h)."""
+    lib = _native.load()
+    d = torch.empty((128, 16 if mode == 2 else 128), device=a.device, dtype=torch.float32)
+    _native.check(lib.b200attn_selftest_umma(mode, _ptr(a), _ptr(b), _ptr(d),
+                                             torch.cuda.current_stream(a.device).cuda_stream))
+    return d
+
+
+def default_scale(head_dim: int) -> float:
+    return 1.0 / math.sqrt(head_dim)

@@ -1,0 +1,433 @@
+// capi.cu — extern "C" entry points of libb200attn.so (declared in include/b200attn.h).
+//
+// Host responsibilities only: validate, pick the compiled template variant for a config,
+// encode TMA tensor maps (cuTensorMapEncodeTiled via the runtime's driver entry point, so the
+// library does not link libcuda), size the split-KV grid, and launch on the caller's stream.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/b200attn.h"
+#include "decode_sm100.cuh"
+#include "prefill_sm100.cuh"
+#include "selftest_sm100.cuh"
+
+namespace {
+
+constexpr int kMaxSmem = 232448;  // 227 KB opt-in per CTA on sm_100a
+constexpr int kNumSMs = 148;
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(B200ATTN_CUDA_ERROR, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+void copy_reason(char* dst, size_t n) {
+  if (dst && n) {
+    strncpy(dst, g_err, n - 1);
+    dst[n - 1] = 0;
+  }
+}
+
+// ------------------------------------------------------------------ tensor maps
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 3-D bf16 map over [d2][d1][d0] (d0 contiguous) with a {64, box1, box2} SWIZZLE_128B box.
+int make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
+                uint64_t stride2_bytes, uint32_t box1, uint32_t box2) {
+  auto fn = encode_fn();
+  if (!fn) return fail(B200ATTN_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {64, box1, box2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(B200ATTN_BAD_ARGS, "cuTensorMapEncodeTiled failed (%d): dims {%llu,%llu,%llu} box {64,%u,%u}",
+                static_cast<int>(r), (unsigned long long)d0, (unsigned long long)d1, (unsigned long long)d2, box1,
+                box2);
+  return B200ATTN_OK;
+}
+
+// ------------------------------------------------------------------ prefill variants
+using PrefillLauncher = int (*)(const b200attn_prefill_params*, cudaStream_t);
+
+template <int NQ, int BN, int NS>
+int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
+  using C = b200::PrefillCfg<NQ, BN, NS>;
+  auto kern = b200::prefill_fwd_kernel<NQ, BN, NS>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(prefill)");
+    attr_done = true;
+  }
+  const int D = 128;
+  CUtensorMap mq, mk, mv;
+  int rc;
+  if ((rc = make_map_3d(&mq, p->q, D, p->num_q_heads, p->total_tokens, D * 2ull, (uint64_t)p->num_q_heads * D * 2,
+                        1, C::BM)))
+    return rc;
+  if ((rc = make_map_3d(&mk, p->k, D, p->num_kv_heads, p->total_tokens, D * 2ull,
+                        (uint64_t)p->num_kv_heads * D * 2, 1, BN)))
+    return rc;
+  if ((rc = make_map_3d(&mv, p->v, D, p->num_kv_heads, p->total_tokens, D * 2ull,
+                        (uint64_t)p->num_kv_heads * D * 2, 1, BN)))
+    return rc;
+  b200::PrefillKernelArgs a;
+  a.cu_seqlens = p->cu_seqlens;
+  a.o = reinterpret_cast<__nv_bfloat16*>(p->o);
+  a.lse = p->lse;
+  a.total_tokens = p->total_tokens;
+  a.num_q_heads = p->num_q_heads;
+  a.group = p->num_q_heads / p->num_kv_heads;
+  a.causal = p->causal;
+  const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / sqrtf((float)p->head_dim);
+  a.scale_log2 = scale * 1.4426950408889634f;
+  const int max_qblk = (p->max_seqlen + C::BM - 1) / C::BM;
+  dim3 grid(p->num_q_heads / NQ, max_qblk, p->num_seqs);
+  kern<<<grid, C::NTHREADS, C::SMEM_BYTES, stream>>>(mq, mk, mv, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
+  return B200ATTN_OK;
+}
+
+struct PrefillEntry {
+  int nq, bn, ns;
+  PrefillLauncher fn;
+  int smem;
+};
+
+#define PF(NQ, BN, NS) {NQ, BN, NS, &launch_prefill<NQ, BN, NS>, b200::PrefillCfg<NQ, BN, NS>::SMEM_BYTES}
+const PrefillEntry kPrefill[] = {
+    PF(2, 128, 2), PF(2, 128, 3), PF(2, 64, 2), PF(2, 64, 3), PF(2, 64, 4),
+    PF(1, 128, 2), PF(1, 128, 3), PF(1, 128, 4), PF(1, 64, 2), PF(1, 64, 3), PF(1, 64, 4),
+};
+#undef PF
+
+int prefill_smem_bytes(int nq, int bn, int ns) {
+  // same formula as PrefillCfg (kept here so unsupported stage counts can be diagnosed)
+  const int q = nq * 128 * 128 * 2, kv = ns * bn * 128 * 2, pb = nq * 128 * bn * 2;
+  return q + kv + pb + (1 + 2 * ns + 2 * nq + 1) * 8 + 16 + 1024;
+}
+
+int check_prefill(const b200attn_prefill_params* p, const b200attn_prefill_variant* v, const PrefillEntry** out) {
+  if (!p || !v) return fail(B200ATTN_BAD_ARGS, "null params/variant");
+  if (v->block_m != 128 && v->block_m != 256)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG,
+                "BLOCK_M=%d: a tcgen05 cta_group::1 Q tile is 128 rows; BLOCK_M must be 128 (1 tile) or 256 "
+                "(2 q heads x 128 rows)",
+                v->block_m);
+  if (v->block_n != 64 && v->block_n != 128)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "BLOCK_N=%d: compiled K/V tiles are 64 or 128 rows", v->block_n);
+  if (v->num_warps != 4)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG,
+                "num_warps=%d: the softmax warpgroup is 4 warps (one thread per TMEM lane of the 128-row tile)",
+                v->num_warps);
+  if (v->waves_per_eu != 1)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG,
+                "waves_per_eu=%d: AMD occupancy hint; one attention CTA owns an SM's TMEM on sm_100a",
+                v->waves_per_eu);
+  const int nq = v->block_m / 128;
+  if (v->num_stages < 2)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "num_stages=%d: the K/V ring needs >= 2 slots", v->num_stages);
+  const int smem = prefill_smem_bytes(nq, v->block_n, v->num_stages);
+  if (smem > kMaxSmem)
+    return fail(B200ATTN_SMEM_OVERFLOW, "shared memory %d B > %d B (BLOCK_M=%d BLOCK_N=%d num_stages=%d)", smem,
+                kMaxSmem, v->block_m, v->block_n, v->num_stages);
+  const PrefillEntry* e = nullptr;
+  for (const auto& x : kPrefill)
+    if (x.nq == nq && x.bn == v->block_n && x.ns == v->num_stages) e = &x;
+  if (!e)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "no compiled variant for BLOCK_M=%d BLOCK_N=%d num_stages=%d",
+                v->block_m, v->block_n, v->num_stages);
+  if (p->head_dim != 128) return fail(B200ATTN_UNSUPPORTED_CONFIG, "head_dim=%d (compiled for 128)", p->head_dim);
+  if (p->num_kv_heads <= 0 || p->num_q_heads <= 0 || p->num_q_heads % p->num_kv_heads)
+    return fail(B200ATTN_BAD_ARGS, "num_q_heads=%d not a multiple of num_kv_heads=%d", p->num_q_heads,
+                p->num_kv_heads);
+  const int group = p->num_q_heads / p->num_kv_heads;
+  if (nq == 2 && group % 2)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG,
+                "BLOCK_M=256 pairs two q heads of one kv head; GQA group %d is odd", group);
+  if (p->num_seqs <= 0 || p->num_seqs > 65535 || p->total_tokens < 0 || p->max_seqlen < 0)
+    return fail(B200ATTN_BAD_ARGS, "num_seqs=%d total_tokens=%d max_seqlen=%d", p->num_seqs, p->total_tokens,
+                p->max_seqlen);
+  if ((p->max_seqlen + 127) / 128 > 65535) return fail(B200ATTN_BAD_ARGS, "max_seqlen too large");
+  *out = e;
+  return B200ATTN_OK;
+}
+
+// ------------------------------------------------------------------ decode variants
+using DecodeLauncher = int (*)(const b200attn_decode_params*, int splits, int tps, cudaStream_t);
+
+template <int NS>
+int launch_decode(const b200attn_decode_params* p, int splits, int tps, cudaStream_t stream) {
+  using C = b200::DecodeCfg<NS>;
+  auto kern = b200::decode_split_kernel<NS>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode)");
+    attr_done = true;
+  }
+  const int D = 128, G = p->num_q_heads / p->num_kv_heads;
+  CUtensorMap mq, mk, mv;
+  int rc;
+  if ((rc = make_map_3d(&mq, p->q, D, p->num_q_heads, p->batch, D * 2ull, (uint64_t)p->num_q_heads * D * 2, G, 1)))
+    return rc;
+  const uint64_t tokens = (uint64_t)p->num_blocks * p->block_size;
+  if ((rc = make_map_3d(&mk, p->k_cache, D, p->num_kv_heads, tokens, D * 2ull, (uint64_t)p->num_kv_heads * D * 2, 1,
+                        p->block_size)))
+    return rc;
+  if ((rc = make_map_3d(&mv, p->v_cache, D, p->num_kv_heads, tokens, D * 2ull, (uint64_t)p->num_kv_heads * D * 2, 1,
+                        p->block_size)))
+    return rc;
+  b200::DecodeKernelArgs a;
+  a.block_table = p->block_table;
+  a.seq_lens = p->seq_lens;
+  a.o = reinterpret_cast<__nv_bfloat16*>(p->o);
+  const size_t rows = (size_t)p->batch * p->num_q_heads;
+  a.part_o = reinterpret_cast<float*>(p->workspace);
+  a.part_ml = a.part_o ? a.part_o + rows * splits * D : nullptr;
+  a.num_q_heads = p->num_q_heads;
+  a.group = G;
+  a.block_size = p->block_size;
+  a.max_blocks = p->max_blocks_per_seq;
+  a.num_blocks = p->num_blocks;
+  a.num_splits = splits;
+  a.tiles_per_split = tps;
+  const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / sqrtf((float)p->head_dim);
+  a.scale_log2 = scale * 1.4426950408889634f;
+  dim3 grid(splits, p->num_kv_heads, p->batch);
+  kern<<<grid, C::NTHREADS, C::SMEM_BYTES, stream>>>(mq, mk, mv, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "decode launch");
+  if (splits > 1) {
+    b200::decode_combine_kernel<<<(unsigned)rows, 128, 0, stream>>>(a.part_o, a.part_ml,
+                                                                    reinterpret_cast<__nv_bfloat16*>(p->o), splits);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "combine launch");
+  }
+  return B200ATTN_OK;
+}
+
+struct DecodeEntry {
+  int ns;
+  DecodeLauncher fn;
+  int smem;
+};
+#define DF(NS) {NS, &launch_decode<NS>, b200::DecodeCfg<NS>::SMEM_BYTES}
+const DecodeEntry kDecode[] = {DF(2), DF(3), DF(4), DF(5), DF(6)};
+#undef DF
+
+int decode_ctas_per_sm(int smem) {
+  const int per_sm = 233472;  // 228 KB per SM
+  int n = per_sm / (smem + 1024);
+  return n < 1 ? 1 : n;
+}
+
+// Resolve the split factor: explicit, or enough CTAs for ~4 waves of the SMs.
+void resolve_splits(const b200attn_decode_params* p, const b200attn_decode_variant* v, int smem, int* splits,
+                    int* tps) {
+  const int tiles = (p->max_seq_len + 127) / 128;
+  int s = v->num_splits;
+  if (s <= 0) {
+    const int units = p->batch * p->num_kv_heads;
+    const int slots = kNumSMs * decode_ctas_per_sm(smem);
+    s = 1;
+    while (s < tiles && units * s < 2 * slots) s *= 2;
+  }
+  if (s > tiles) s = tiles > 0 ? tiles : 1;
+  int t = (tiles + s - 1) / s;
+  if (t < 1) t = 1;
+  s = (tiles + t - 1) / t;  // drop empty trailing splits
+  if (s < 1) s = 1;
+  *splits = s;
+  *tps = t;
+}
+
+int check_decode(const b200attn_decode_params* p, const b200attn_decode_variant* v, const DecodeEntry** out) {
+  if (!p || !v) return fail(B200ATTN_BAD_ARGS, "null params/variant");
+  if (v->tile_n != 128) return fail(B200ATTN_UNSUPPORTED_CONFIG, "tile_n=%d (compiled for 128)", v->tile_n);
+  const DecodeEntry* e = nullptr;
+  for (const auto& x : kDecode)
+    if (x.ns == v->num_stages) e = &x;
+  if (!e) return fail(B200ATTN_UNSUPPORTED_CONFIG, "num_stages=%d has no compiled decode variant", v->num_stages);
+  if (e->smem > kMaxSmem) return fail(B200ATTN_SMEM_OVERFLOW, "decode smem %d B", e->smem);
+  if (v->num_splits < 0 || v->num_splits > 1024) return fail(B200ATTN_BAD_ARGS, "num_splits=%d", v->num_splits);
+  if (p->head_dim != 128) return fail(B200ATTN_UNSUPPORTED_CONFIG, "head_dim=%d (compiled for 128)", p->head_dim);
+  if (p->num_kv_heads <= 0 || p->num_q_heads % p->num_kv_heads)
+    return fail(B200ATTN_BAD_ARGS, "num_q_heads=%d not a multiple of num_kv_heads=%d", p->num_q_heads,
+                p->num_kv_heads);
+  const int G = p->num_q_heads / p->num_kv_heads;
+  if (G > 16) return fail(B200ATTN_UNSUPPORTED_CONFIG, "GQA group %d > 16 (MMA N padded to 16)", G);
+  const int bs = p->block_size;
+  if (bs < 8 || bs > 128 || (bs & (bs - 1)))
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "block_size=%d: pages must be a power of two in [8,128]", bs);
+  if (p->batch <= 0 || p->batch > 65535 || p->num_blocks <= 0 || p->max_blocks_per_seq <= 0)
+    return fail(B200ATTN_BAD_ARGS, "batch=%d num_blocks=%d max_blocks_per_seq=%d", p->batch, p->num_blocks,
+                p->max_blocks_per_seq);
+  if (p->max_seq_len > p->max_blocks_per_seq * bs)
+    return fail(B200ATTN_BAD_ARGS, "max_seq_len=%d exceeds block_table capacity %d", p->max_seq_len,
+                p->max_blocks_per_seq * bs);
+  *out = e;
+  return B200ATTN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int b200attn_abi_version(void) { return B200ATTN_ABI_VERSION; }
+
+const char* b200attn_build_info(void) {
+  return "b200attn sm_100a (tcgen05/TMEM/TMA)";
+}
+
+const char* b200attn_status_string(int s) {
+  switch (s) {
+    case B200ATTN_OK: return "ok";
+    case B200ATTN_UNSUPPORTED_CONFIG: return "unsupported_config";
+    case B200ATTN_SMEM_OVERFLOW: return "smem_overflow";
+    case B200ATTN_TMEM_OVERFLOW: return "tmem_overflow";
+    case B200ATTN_BAD_ARGS: return "bad_args";
+    case B200ATTN_CUDA_ERROR: return "cuda_error";
+  }
+  return "unknown";
+}
+
+const char* b200attn_last_error(void) { return g_err; }
+
+int b200attn_prefill_supported(const b200attn_prefill_params* p, const b200attn_prefill_variant* v, char* reason,
+                               size_t n) {
+  const PrefillEntry* e;
+  g_err[0] = 0;
+  int rc = check_prefill(p, v, &e);
+  copy_reason(reason, n);
+  return rc;
+}
+
+int b200attn_prefill(const b200attn_prefill_params* p, const b200attn_prefill_variant* v, void* stream) {
+  const PrefillEntry* e;
+  g_err[0] = 0;
+  int rc = check_prefill(p, v, &e);
+  if (rc) return rc;
+  if (!p->q || !p->k || !p->v || !p->o || !p->cu_seqlens) return fail(B200ATTN_BAD_ARGS, "null tensor pointer");
+  if (p->total_tokens == 0 || p->max_seqlen == 0) return B200ATTN_OK;
+  return e->fn(p, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int b200attn_decode_supported(const b200attn_decode_params* p, const b200attn_decode_variant* v, char* reason,
+                              size_t n) {
+  const DecodeEntry* e;
+  g_err[0] = 0;
+  int rc = check_decode(p, v, &e);
+  copy_reason(reason, n);
+  return rc;
+}
+
+int b200attn_decode_num_splits(const b200attn_decode_params* p, const b200attn_decode_variant* v) {
+  const DecodeEntry* e;
+  if (check_decode(p, v, &e)) return -1;
+  int s, t;
+  resolve_splits(p, v, e->smem, &s, &t);
+  return s;
+}
+
+size_t b200attn_decode_workspace_size(const b200attn_decode_params* p, const b200attn_decode_variant* v) {
+  const DecodeEntry* e;
+  if (check_decode(p, v, &e)) return 0;
+  int s, t;
+  resolve_splits(p, v, e->smem, &s, &t);
+  if (s <= 1) return 0;
+  const size_t rows = (size_t)p->batch * p->num_q_heads;
+  return rows * s * (128 + 2) * sizeof(float);
+}
+
+int b200attn_decode(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream) {
+  const DecodeEntry* e;
+  g_err[0] = 0;
+  int rc = check_decode(p, v, &e);
+  if (rc) return rc;
+  if (!p->q || !p->k_cache || !p->v_cache || !p->block_table || !p->seq_lens || !p->o)
+    return fail(B200ATTN_BAD_ARGS, "null tensor pointer");
+  int s, t;
+  resolve_splits(p, v, e->smem, &s, &t);
+  if (s > 1) {
+    const size_t need = (size_t)p->batch * p->num_q_heads * s * (128 + 2) * sizeof(float);
+    if (!p->workspace || p->workspace_bytes < need)
+      return fail(B200ATTN_BAD_ARGS, "workspace %zu B < %zu B needed for %d splits", p->workspace_bytes, need, s);
+  }
+  return e->fn(p, s, t, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int b200attn_combine(const float* part_o, const float* part_ml, void* o, int32_t rows, int32_t num_splits,
+                     void* stream) {
+  g_err[0] = 0;
+  if (!part_o || !part_ml || !o || rows <= 0 || num_splits <= 0) return fail(B200ATTN_BAD_ARGS, "combine args");
+  b200::decode_combine_kernel<<<rows, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      part_o, part_ml, reinterpret_cast<__nv_bfloat16*>(o), num_splits);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? B200ATTN_OK : cuda_fail(e, "combine launch");
+}
+
+int b200attn_cache_append(const void* new_k, const void* new_v, void* k_cache, void* v_cache,
+                          const int64_t* slot_mapping, int32_t num_tokens, int32_t num_kv_heads, int32_t head_dim,
+                          int32_t block_size, int32_t num_blocks, void* stream) {
+  g_err[0] = 0;
+  if (head_dim != 128) return fail(B200ATTN_UNSUPPORTED_CONFIG, "head_dim=%d (compiled for 128)", head_dim);
+  if (!new_k || !new_v || !k_cache || !v_cache || !slot_mapping || num_tokens < 0 || num_kv_heads <= 0)
+    return fail(B200ATTN_BAD_ARGS, "cache_append args");
+  if (num_tokens == 0) return B200ATTN_OK;
+  const long long warps = (long long)num_tokens * num_kv_heads;
+  const int threads = 256;
+  const long long blocks = (warps * 32 + threads - 1) / threads;
+  b200::cache_append_kernel<<<(unsigned)blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const uint4*>(new_k), reinterpret_cast<const uint4*>(new_v), reinterpret_cast<uint4*>(k_cache),
+      reinterpret_cast<uint4*>(v_cache), slot_mapping, num_tokens, num_kv_heads,
+      (int64_t)num_blocks * block_size);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? B200ATTN_OK : cuda_fail(e, "cache_append launch");
+}
+
+int b200attn_selftest_umma(int mode, const void* a, const void* b, float* d, void* stream) {
+  g_err[0] = 0;
+  if (mode < 0 || mode > 2 || !a || !b || !d) return fail(B200ATTN_BAD_ARGS, "selftest args");
+  cudaError_t ea = cudaFuncSetAttribute(b200::umma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        b200::kSelftestSmem);
+  if (ea != cudaSuccess) return cuda_fail(ea, "cudaFuncSetAttribute(selftest)");
+  b200::umma_selftest_kernel<<<1, 128, b200::kSelftestSmem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(a), reinterpret_cast<const __nv_bfloat16*>(b), d, mode);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? B200ATTN_OK : cuda_fail(e, "selftest launch");
+}
+
+}  // extern "C"

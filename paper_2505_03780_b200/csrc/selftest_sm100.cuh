@@ -1,0 +1,98 @@
+// selftest_sm100.cuh — one-CTA tcgen05 GEMM that exercises exactly the descriptor / swizzle
+// encodings the attention kernels use (K-major and MN-major SWIZZLE_128B operands, M=128 with
+// N=128 and N=16), with operands staged by plain threads so TMA is not involved.
+#pragma once
+#include "sm100_common.cuh"
+
+namespace b200 {
+
+constexpr int kSelftestSmem = 2 * 128 * 128 * 2 + 16 + 1024;
+
+// byte offset of element (row, col) in a K-major SW128 tile with `rows` rows (col = K index)
+__device__ __forceinline__ uint32_t sw128_kmajor(int row, int col, int rows) {
+  return (col >> 6) * rows * 128 + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4) + (col & 7) * 2;
+}
+
+__global__ void __launch_bounds__(128) umma_selftest_kernel(const __nv_bfloat16* A, const __nv_bfloat16* B,
+                                                            float* D, int mode) {
+  extern __shared__ uint8_t st_raw[];
+  uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(st_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sA + 128 * 128 * 2;
+  uint64_t& bar = *reinterpret_cast<uint64_t*>(sB + 128 * 128 * 2);
+  uint32_t& tslot = *reinterpret_cast<uint32_t*>(sB + 128 * 128 * 2 + 8);
+  const int tid = threadIdx.x;
+  // A: modes 0/1 K-major [M=128][K=128]; mode 2 MN-major given as [K][M] (same swizzle formula
+  // with the 128-B rows running along M).
+  for (int i = tid; i < 128 * 128; i += 128) {
+    const int r = i / 128, c = i % 128;
+    *reinterpret_cast<__nv_bfloat16*>(sA + sw128_kmajor(r, c, 128)) = A[i];
+  }
+  const int brows = (mode == 2) ? 16 : 128;
+  for (int i = tid; i < brows * 128; i += 128) {
+    const int r = i / 128, c = i % 128;
+    *reinterpret_cast<__nv_bfloat16*>(sB + sw128_kmajor(r, c, brows)) = B[i];
+  }
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (tid < 32) tmem_alloc(&tslot, 128);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const int N = (mode == 2) ? 16 : 128;
+  if (tid == 0) {
+    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+    const uint32_t idesc = idesc_bf16_f32(128, N, mode == 2, mode == 1);
+    for (int kk = 0; kk < 8; ++kk) {
+      uint64_t da, db;
+      if (mode == 2) da = sdesc_sw128(a0 + kk * 2048, 16384, 1024);
+      else da = sdesc_sw128(a0 + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+      if (mode == 1) db = sdesc_sw128(b0 + kk * 2048, 16384, 1024);
+      else db = sdesc_sw128(b0 + (kk >> 2) * brows * 128 + (kk & 3) * 32, 16, 1024);
+      umma_ss(tmem, da, db, idesc, kk > 0);
+    }
+    umma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  const uint32_t taddr = tmem + (static_cast<uint32_t>((tid >> 5) << 5) << 16);
+  if (N == 16) {
+    uint32_t r[16];
+    tmem_ld16(taddr, r);
+    for (int j = 0; j < 16; ++j) D[tid * 16 + j] = __uint_as_float(r[j]);
+  } else {
+    for (int c = 0; c < 4; ++c) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c * 32, r);
+      for (int j = 0; j < 32; ++j) D[tid * 128 + c * 32 + j] = __uint_as_float(r[j]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 128);
+  }
+}
+
+// Paged KV-cache append: one warp per (token, kv head), 16-B vectors (128 x bf16 = 256 B row).
+__global__ void cache_append_kernel(const uint4* __restrict__ nk, const uint4* __restrict__ nv,
+                                    uint4* __restrict__ kc, uint4* __restrict__ vc,
+                                    const int64_t* __restrict__ slots, int num_tokens, int kv_heads,
+                                    int64_t num_slots) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= num_tokens * kv_heads) return;
+  const int tok = w / kv_heads, h = w % kv_heads;
+  const int64_t slot = slots[tok];
+  if (slot < 0 || slot >= num_slots) return;
+  const int64_t src = (static_cast<int64_t>(tok) * kv_heads + h) * 16;  // 16 uint4 per 128-wide row
+  const int64_t dst = (slot * kv_heads + h) * 16;
+  if (lane < 16) kc[dst + lane] = nk[src + lane];
+  else vc[dst + lane - 16] = nv[src + lane - 16];
+}
+
+}  // namespace b200

@@ -1,0 +1,102 @@
+"""Per-shape dispatch table: the offline sweep's answer to "which compiled variant for this shape".
+
+The paper's in-process Triton autotuning is replaced by an offline sweep (ktune ``tune`` driving
+``python -m paper_2505_03780_b200.runner``) whose best configs are exported as a ktune cache bundle
+(ref/pkg/src/ktune/cache.py:291-322; entry format ref/pkg/README.md "Result / cache entry").
+``load_table`` folds such a bundle (or a directory of ``*.result.json`` entries) into
+{op: [(dims, best_config), ...]}; lookups pick the exact shape or else the nearest tuned shape
+of the same op and head geometry (log-distance over batch_size and seq_len).
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+from pathlib import Path
+from typing import Optional
+
+PKG_DIR = Path(__file__).resolve().parent
+DEFAULT_TABLE = PKG_DIR / "dispatch_table.json"
+
+# fixed defaults: what a user gets without a sweep (and the C5 "fixed default" for prefill
+# is SURVEY §8(d)'s BLOCK_M=128, BLOCK_N=128, num_warps=4, num_stages=2, waves_per_eu=1).
+PREFILL_DEFAULT = {"BLOCK_M": 256, "BLOCK_N": 128, "num_warps": 4, "num_stages": 3, "waves_per_eu": 1,
+                   "PRE_LOAD_V": False}
+PREFILL_FIXED_BASELINE = {"BLOCK_M": 128, "BLOCK_N": 128, "num_warps": 4, "num_stages": 2, "waves_per_eu": 1,
+                          "PRE_LOAD_V": False}
+DECODE_DEFAULT = {"num_splits": 0, "num_stages": 4, "TILE_N": 128}
+
+_GEOM = ("num_q_heads", "num_kv_heads", "head_dim", "block_size", "causal")
+
+_table = None
+
+
+def _entries_from(path: Path):
+    doc = json.loads(path.read_text())
+    if isinstance(doc, dict) and "entries" in doc:  # ktune bundle
+        yield from doc["entries"]
+    elif isinstance(doc, dict) and "fingerprint" in doc:  # single cache entry
+        yield doc
+    elif isinstance(doc, dict) and "rows" in doc:  # our compact table
+        for row in doc["rows"]:
+            yield {"shape": row["shape"], "result": {"best": row["best"], "best_median_ms": row.get("median_ms")}}
+
+
+def load_table(path=None) -> dict:
+    path = Path(path or os.environ.get("B200ATTN_DISPATCH", DEFAULT_TABLE))
+    table: dict = {}
+    files = []
+    if path.is_dir():
+        files = sorted(path.glob("*.result.json"))
+    elif path.exists():
+        files = [path]
+    for f in files:
+        for e in _entries_from(f):
+            shape = e.get("shape", {})
+            best = (e.get("result") or {}).get("best")
+            if best and "op" in shape:
+                table.setdefault(shape["op"], []).append((dict(shape), dict(best)))
+    return table
+
+
+def table() -> dict:
+    global _table
+    if _table is None:
+        _table = load_table()
+    return _table
+
+
+def reset():
+    global _table
+    _table = None
+
+
+def lookup(op: str, dims: dict) -> Optional[dict]:
+    rows = table().get(op, [])
+    best, best_d = None, math.inf
+    for shape, cfg in rows:
+        if any(k in shape and k in dims and shape[k] != dims[k] for k in _GEOM):
+            continue
+        d = 0.0
+        for k in ("batch_size", "seq_len"):
+            if k in shape and k in dims and shape[k] and dims[k]:
+                d += abs(math.log2(float(shape[k])) - math.log2(float(dims[k])))
+        if d < best_d:
+            best, best_d = cfg, d
+    return best
+
+
+def default_prefill_config(**dims) -> dict:
+    dims = dict(dims)
+    num_seqs = dims.pop("num_seqs", 1)
+    dims["batch_size"] = num_seqs
+    dims["seq_len"] = dims.get("max_seqlen", 0)
+    cfg = lookup("prefill", dims) or PREFILL_DEFAULT
+    if cfg["BLOCK_M"] == 256 and (dims.get("num_q_heads", 2) // max(dims.get("num_kv_heads", 1), 1)) % 2:
+        cfg = dict(cfg, BLOCK_M=128)  # head pairing needs an even GQA group
+    return dict(cfg)
+
+
+def default_decode_config(**dims) -> dict:
+    return dict(lookup("decode", dims) or DECODE_DEFAULT)

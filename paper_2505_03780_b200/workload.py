@@ -1,0 +1,144 @@
+"""Synthetic attention workloads keyed by a ktune ShapeKey dict.
+
+The reference runner allocates inputs from a binding's tensor recipes
+(ref/pkg/runner/src/ktune_triton_runner/backends.py:119-137: CPU ``torch.Generator(seed)``, fp32
+randn cast to the kernel dtype).  A binding cannot express varlen ``cu_seqlens``, page pools or a
+permuted ``block_table`` (ref/pkg/runner/src/ktune_triton_runner/binding.py:154-163), so the attention
+runner builds them here from the shape dims (SURVEY §8(d) conventions):
+
+  prefill: {"op":"prefill","batch_size","seq_len" | "seq_len_min","seq_len_max","len_dist",
+            "num_q_heads","num_kv_heads","head_dim","causal","dtype","seed"}
+  decode:  {"op":"decode","batch_size","seq_len","num_q_heads","num_kv_heads","head_dim",
+            "block_size","dtype","seed"}
+
+Small tensors follow the reference exactly (CPU generator, fp32 randn -> bf16).  Tensors above
+``CPU_GEN_LIMIT`` elements are drawn from a seeded CUDA generator instead (a 32-GiB paged cache
+cannot be drawn on the host per request); ``gen`` forces either.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+CPU_GEN_LIMIT = 1 << 26
+
+
+def varlen_lengths(shape: dict) -> list[int]:
+    B = int(shape["batch_size"])
+    if "seq_len" in shape:
+        return [int(shape["seq_len"])] * B
+    lo, hi = int(shape["seq_len_min"]), int(shape["seq_len_max"])
+    dist = shape.get("len_dist", "geometric")
+    if B == 1:
+        return [hi]
+    if dist == "geometric":
+        return [int(round(lo * (hi / lo) ** (i / (B - 1)))) for i in range(B)]
+    if dist == "linear":
+        return [int(round(lo + (hi - lo) * i / (B - 1))) for i in range(B)]
+    raise ValueError(f"unknown len_dist {dist!r}")
+
+
+def _randn(shape, gen_kind: str, seed: int, device) -> torch.Tensor:
+    n = 1
+    for s in shape:
+        n *= int(s)
+    kind = gen_kind if gen_kind != "auto" else ("cpu" if n <= CPU_GEN_LIMIT else "cuda")
+    if kind == "cpu":
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        return torch.randn(shape, generator=g, dtype=torch.float32).to(torch.bfloat16).to(device)
+    g = torch.Generator(device=device).manual_seed(seed)
+    out = torch.empty(shape, dtype=torch.bfloat16, device=device)
+    # fill in fp32 chunks to bound the temporary
+    flat = out.view(-1)
+    step = 1 << 27
+    for i in range(0, n, step):
+        m = min(step, n - i)
+        flat[i:i + m] = torch.randn(m, generator=g, dtype=torch.float32, device=device).to(torch.bfloat16)
+    return out
+
+
+@dataclass
+class PrefillInputs:
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
+    cu_seqlens: torch.Tensor
+    max_seqlen: int
+    lens: list
+    causal: bool
+
+    @property
+    def flops(self) -> int:
+        """Algorithmic FLOPs: 4*D*Hq*sum L(L+1)/2 (causal) or 4*D*Hq*sum L^2."""
+        D, Hq = self.q.shape[2], self.q.shape[1]
+        pairs = sum(L * (L + 1) // 2 if self.causal else L * L for L in self.lens)
+        return 4 * D * Hq * pairs
+
+
+@dataclass
+class DecodeInputs:
+    q: torch.Tensor
+    k_cache: torch.Tensor
+    v_cache: torch.Tensor
+    block_table: torch.Tensor
+    seq_lens: torch.Tensor
+    max_seq_len: int
+    lens: list
+
+    @property
+    def kv_bytes(self) -> int:
+        """K+V bytes the decode must read: 2 * sum(n) * Hkv * D * 2."""
+        Hkv, D = self.k_cache.shape[2], self.k_cache.shape[3]
+        return 2 * sum(self.lens) * Hkv * D * 2
+
+    @property
+    def total_bytes(self) -> int:
+        """K+V + Q + O + block_table + seq_lens bytes."""
+        return (self.kv_bytes + 2 * self.q.numel() * 2 + self.block_table.numel() * 4 + self.seq_lens.numel() * 4)
+
+
+def make_prefill(shape: dict, device="cuda", gen: str = "auto", seed: Optional[int] = None) -> PrefillInputs:
+    seed = int(shape.get("seed", 0)) if seed is None else seed
+    lens = varlen_lengths(shape)
+    T = sum(lens)
+    Hq, Hkv, D = int(shape["num_q_heads"]), int(shape["num_kv_heads"]), int(shape["head_dim"])
+    q = _randn((T, Hq, D), gen, seed, device)
+    k = _randn((T, Hkv, D), gen, seed + 1, device)
+    v = _randn((T, Hkv, D), gen, seed + 2, device)
+    cu = torch.zeros(len(lens) + 1, dtype=torch.int32)
+    cu[1:] = torch.cumsum(torch.tensor(lens, dtype=torch.int32), 0)
+    return PrefillInputs(q, k, v, cu.to(device), max(lens) if lens else 0, lens, bool(shape.get("causal", True)))
+
+
+def make_decode(shape: dict, device="cuda", gen: str = "auto", seed: Optional[int] = None,
+                lens: Optional[list] = None, extra_blocks: int = 0) -> DecodeInputs:
+    seed = int(shape.get("seed", 0)) if seed is None else seed
+    B = int(shape["batch_size"])
+    ctx = int(shape["seq_len"])
+    Hq, Hkv, D = int(shape["num_q_heads"]), int(shape["num_kv_heads"]), int(shape["head_dim"])
+    bs = int(shape.get("block_size", 16))
+    lens = list(lens) if lens is not None else [ctx] * B
+    max_blocks = (max(lens) + bs - 1) // bs if lens else 1
+    max_blocks = max(max_blocks, 1)
+    NB = B * max_blocks + extra_blocks
+    q = _randn((B, Hq, D), gen, seed, device)
+    kc = _randn((NB, bs, Hkv, D), gen, seed + 1, device)
+    vc = _randn((NB, bs, Hkv, D), gen, seed + 2, device)
+    g = torch.Generator(device="cpu").manual_seed(seed + 3)
+    perm = torch.randperm(NB, generator=g)[: B * max_blocks].to(torch.int32).reshape(B, max_blocks)
+    return DecodeInputs(q, kc, vc, perm.to(device), torch.tensor(lens, dtype=torch.int32, device=device),
+                        max(lens) if lens else 0, lens)
+
+
+# the BASELINE.json configurations
+C1 = {"op": "prefill", "batch_size": 1, "seq_len": 512, "num_q_heads": 32, "num_kv_heads": 8, "head_dim": 128,
+      "causal": True, "dtype": "bfloat16", "seed": 0}
+C2 = {"op": "decode", "batch_size": 64, "seq_len": 4096, "num_q_heads": 32, "num_kv_heads": 8, "head_dim": 128,
+      "block_size": 16, "dtype": "bfloat16", "seed": 0}
+C3 = {"op": "prefill", "batch_size": 16, "seq_len_min": 128, "seq_len_max": 8192, "len_dist": "geometric",
+      "num_q_heads": 32, "num_kv_heads": 8, "head_dim": 128, "causal": True, "dtype": "bfloat16", "seed": 0}
+C4 = {"op": "decode", "batch_size": 256, "seq_len": 32768, "num_q_heads": 64, "num_kv_heads": 8, "head_dim": 128,
+      "block_size": 16, "dtype": "bfloat16", "seed": 0}
