@@ -1,0 +1,226 @@
+"""Evaluation backends for the attention runner.
+
+``B200Backend`` fills the slot of the reference's ``TritonBackend``
+(ref/pkg/runner/src/ktune_triton_runner/backends.py:72-206): allocate inputs for a shape, launch
+the configured variant, time it.  Differences forced by the hardware/ABI, not by taste:
+  * there is no JIT: every config maps to an AOT-compiled sm_100a template instance or is
+    rejected up front (``status: invalid`` with the reason from the C ABI), the analogue of
+    "configurations the device rejects" (backends.py:200-205);
+  * ``compile_ms`` is the cold first launch (function attributes, TMA descriptor encode, module
+    load), measured the same way as the reference's cold JIT launch (backends.py:167-172);
+  * inputs are built once per shape and cached (the reference re-draws them per request on the
+    host, backends.py:119-137, which is prohibitive for a 32-GiB paged cache);
+  * timing is identical: CUDA-graph capture, then one event pair + synchronize per rep
+    (backends.py:174-196), capability ``graph-timing``.
+Sticky device faults (illegal address etc.) are reported as ``error`` and the process exits so
+ktune respawns a clean runner (ref/pkg/src/ktune/executor.py:540-552).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import importlib.metadata as md
+import time
+
+from .. import _native, __version__
+from .binding import AttentionBinding
+
+MAX_PREFILL_TOKENS = 1 << 21  # larger prefill shapes are shape-invalid
+
+
+class EvaluationOutcome:
+    def __init__(self, status, compile_ms=0.0, latencies_ms=(), reason="", fatal=False):
+        self.status = status
+        self.compile_ms = compile_ms
+        self.latencies_ms = list(latencies_ms)
+        self.reason = reason
+        self.fatal = fatal
+
+    @classmethod
+    def ok(cls, compile_ms, latencies_ms):
+        return cls("ok", compile_ms=compile_ms, latencies_ms=latencies_ms)
+
+    @classmethod
+    def invalid(cls, reason):
+        return cls("invalid", reason=reason)
+
+    @classmethod
+    def error(cls, reason, fatal=False):
+        return cls("error", reason=reason, fatal=fatal)
+
+
+def _pkg_version(name: str) -> str:
+    try:
+        return md.version(name)
+    except md.PackageNotFoundError:
+        return "none"
+
+
+class StubBackend:
+    """GPU-free stand-in with deterministic positive latencies (protocol tests only)."""
+
+    capability = "stub-timing"
+
+    def __init__(self, binding: AttentionBinding, device: int = 0):
+        self.binding = binding
+
+    def fingerprint_fields(self) -> dict:
+        return {"device_name": "stub-device", "driver_version": "stub", "toolchain_version": f"stub-{__version__}"}
+
+    def evaluate(self, config: dict, shape: dict, warmups: int, reps: int) -> EvaluationOutcome:
+        material = repr(sorted(config.items())) + repr(sorted(shape.items()))
+        bucket = int.from_bytes(hashlib.sha256(material.encode()).digest()[:4], "big")
+        return EvaluationOutcome.ok(1.0, [0.25 + (bucket % 1000) / 1000.0] * reps)
+
+
+class B200Backend:
+    capability = "graph-timing"
+
+    def __init__(self, binding: AttentionBinding, device: int = 0):
+        self.binding = binding
+        self.device_index = device
+        _native.load()  # fail at startup, not at the first request, if the library is missing
+        self._dev_name, self._driver = self._query_device(device)
+        self._torch = None
+        self._shape_key = None
+        self._inputs = None
+
+    @staticmethod
+    def _query_device(idx: int):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            name = pynvml.nvmlDeviceGetName(h)
+            drv = pynvml.nvmlSystemGetDriverVersion()
+            name = name.decode() if isinstance(name, bytes) else name
+            drv = drv.decode() if isinstance(drv, bytes) else drv
+            return name, drv
+        except Exception as e:  # NVML absent -> no GPU visible
+            raise RuntimeError(f"no NVIDIA device visible via NVML: {e}") from None
+
+    def fingerprint_fields(self) -> dict:
+        return {
+            "device_name": self._dev_name,
+            "driver_version": self._driver,
+            "toolchain_version": f"nvcc-12.9+sm_100a+torch-{_pkg_version('torch')}",
+        }
+
+    # -- workload ------------------------------------------------------------------------
+    def _setup_torch(self):
+        if self._torch is None:
+            import torch
+
+            torch.cuda.set_device(self.device_index)
+            self._torch = torch
+        return self._torch
+
+    def _inputs_for(self, shape: dict):
+        from .. import workload
+
+        key = repr(sorted(shape.items()))
+        if key != self._shape_key:
+            self._inputs = None  # free the previous shape first (a 32-GiB cache must not double up)
+            self._torch.cuda.empty_cache()
+            shape = dict(shape)
+            shape.setdefault("seed", self.binding.seed)
+            if self.binding.op == "prefill":
+                self._inputs = workload.make_prefill(shape, device="cuda")
+            else:
+                self._inputs = workload.make_decode(shape, device="cuda")
+            self._shape_key = key
+        return self._inputs
+
+    def _launcher(self, config: dict, x):
+        from .. import attention as A
+
+        torch = self._torch
+        if self.binding.op == "prefill":
+            out = torch.empty_like(x.q)
+            return lambda: A.prefill_varlen(x.q, x.k, x.v, x.cu_seqlens, x.max_seqlen, out=out, causal=x.causal,
+                                            config=config)
+        out = torch.empty_like(x.q)
+        return lambda: A.paged_decode(x.q, x.k_cache, x.v_cache, x.block_table, x.seq_lens,
+                                      max_seq_len=x.max_seq_len, out=out, config=config)
+
+    def _precheck(self, config: dict, shape: dict):
+        """Config/shape validity without allocating (C-ABI *_supported)."""
+        from .. import attention as A
+        from .. import workload
+
+        op = shape.get("op", self.binding.op)
+        if op != self.binding.op:
+            return f"this runner serves op {self.binding.op!r}, shape asks for {op!r}"
+        Hq, Hkv, D = int(shape["num_q_heads"]), int(shape["num_kv_heads"]), int(shape["head_dim"])
+        if self.binding.op == "prefill":
+            lens = workload.varlen_lengths(shape)
+            if sum(lens) > MAX_PREFILL_TOKENS:
+                return f"shape has {sum(lens)} tokens > {MAX_PREFILL_TOKENS} (q/k/v/o would not fit one GPU)"
+            rc, why = A.prefill_supported((sum(lens), Hq, D), Hkv, len(lens), max(lens), config,
+                                          causal=bool(shape.get("causal", True)))
+        else:
+            B, ctx, bs = int(shape["batch_size"]), int(shape["seq_len"]), int(shape.get("block_size", 16))
+            mb = (ctx + bs - 1) // bs
+            rc, why = A.decode_supported((B, Hq, D), (B * mb, bs, Hkv, D), mb, ctx, config)
+        if rc in _native.INVALID_CODES:
+            return why
+        if rc != _native.OK:
+            raise _native.B200AttnError(rc, why)
+        return None
+
+    def evaluate(self, config: dict, shape: dict, warmups: int, reps: int) -> EvaluationOutcome:
+        torch = self._setup_torch()
+        try:
+            why = self._precheck(config, shape)
+            if why:
+                return EvaluationOutcome.invalid(why)
+            x = self._inputs_for(shape)
+            launch = self._launcher(config, x)
+            torch.cuda.synchronize()
+            t0 = time.monotonic()
+            launch()  # cold launch: attributes, tensor-map encode, module load
+            torch.cuda.synchronize()
+            compile_ms = (time.monotonic() - t0) * 1000.0
+            replay = launch
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    launch()
+                replay = g.replay
+            except RuntimeError:
+                replay = launch
+            for _ in range(warmups):
+                replay()
+            torch.cuda.synchronize()
+            lat = []
+            for _ in range(reps):
+                s = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True)
+                s.record()
+                replay()
+                e.record()
+                torch.cuda.synchronize()
+                lat.append(s.elapsed_time(e))
+            if any(not (v > 0) for v in lat):
+                return EvaluationOutcome.error("device reported a non-positive latency")
+            return EvaluationOutcome.ok(compile_ms, lat)
+        except _native.B200AttnError as e:
+            if e.invalid:
+                return EvaluationOutcome.invalid(str(e))
+            return EvaluationOutcome.error(str(e), fatal=e.status == _native.CUDA_ERROR)
+        except torch.cuda.OutOfMemoryError as e:
+            self._inputs, self._shape_key = None, None
+            return EvaluationOutcome.invalid(f"OutOfMemoryError: {e}")
+        except RuntimeError as e:
+            text = str(e)
+            sticky = any(s in text for s in ("illegal", "unspecified launch failure", "misaligned", "trap"))
+            return EvaluationOutcome.error(f"{type(e).__name__}: {text}", fatal=sticky)
+
+
+def make_backend(name: str, binding: AttentionBinding, device: int = 0):
+    if name == "stub":
+        return StubBackend(binding, device)
+    if name == "b200":
+        return B200Backend(binding, device)
+    raise ValueError(f"unknown backend {name!r}")

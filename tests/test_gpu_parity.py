@@ -1,0 +1,345 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) vs the CPU oracle on identical inputs.
+
+Tolerance (bf16 in, fp32 accumulate, bf16 out), per case:
+  * max-abs error <= 2 x (max-abs error of torch SDPA run in bf16 on the same inputs) + 1e-4, and
+  * max-rel error  = max |out - ref| / max(|ref|, 1)  <= 1e-2.
+Errors are printed per case (pytest -s) so the report has the numbers.
+Full-size configs (C2, C3, C4-shard) are checked on seeded subsets against the oracle (heads and
+sequences are independent, so a slice is an exact sub-problem) and through size-independent
+properties: split-count invariance, physical-page permutation invariance (bit-exact).
+"""
+import glob
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+import oracle
+from paper_2505_03780_b200 import attention as A
+from paper_2505_03780_b200 import workload as W
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+DEV = "cuda"
+
+
+def pcfg(bm=256, bn=128, ns=3, pre=False):
+    return dict(BLOCK_M=bm, BLOCK_N=bn, num_warps=4, num_stages=ns, waves_per_eu=1, PRE_LOAD_V=pre)
+
+
+def dcfg(splits=0, ns=4):
+    return dict(num_splits=splits, num_stages=ns, TILE_N=128)
+
+
+def sdpa_prefill_bf16(q, k, v, cu, causal):
+    outs = []
+    G = q.shape[1] // k.shape[1]
+    for s in range(len(cu) - 1):
+        a, b = int(cu[s]), int(cu[s + 1])
+        if b == a:
+            continue
+        qq = q[a:b].transpose(0, 1)[None]
+        kk = k[a:b].repeat_interleave(G, 1).transpose(0, 1)[None]
+        vv = v[a:b].repeat_interleave(G, 1).transpose(0, 1)[None]
+        outs.append(F.scaled_dot_product_attention(qq, kk, vv, is_causal=causal)[0].transpose(0, 1))
+    return torch.cat(outs).float().cpu().numpy()
+
+
+def sdpa_decode_bf16(q, kc, vc, bt, sl):
+    B, Hq, D = q.shape
+    G = Hq // kc.shape[2]
+    bs = kc.shape[1]
+    out = torch.zeros(B, Hq, D)
+    for b in range(B):
+        n = int(sl[b])
+        t = torch.arange(n, device=q.device)
+        pages = bt[b, t // bs].long()
+        kk = kc[pages, t % bs].repeat_interleave(G, 1).transpose(0, 1)[None]
+        vv = vc[pages, t % bs].repeat_interleave(G, 1).transpose(0, 1)[None]
+        out[b] = F.scaled_dot_product_attention(q[b][None, :, None], kk, vv)[0, :, 0].float().cpu()
+    return out.numpy()
+
+
+def check(name, out, ref, base):
+    out = out.float().cpu().numpy() if isinstance(out, torch.Tensor) else out
+    err = np.abs(out - ref)
+    base_err = np.abs(base - ref).max()
+    rel = (err / np.maximum(np.abs(ref), 1.0)).max()
+    print(f"[parity] {name}: max_abs={err.max():.3e} max_rel={rel:.3e} mean_abs={err.mean():.2e} "
+          f"sdpa_bf16_max_abs={base_err:.3e}")
+    assert not np.isnan(out).any(), name
+    assert err.max() <= 2 * base_err + 1e-4, (name, err.max(), base_err)
+    assert rel <= 1e-2, (name, rel)
+
+
+def run_prefill(lens, Hq=32, Hkv=8, causal=True, cfg=None, seed=1):
+    g = torch.Generator().manual_seed(seed)
+    T = sum(lens)
+    q = torch.randn(T, Hq, 128, generator=g).bfloat16()
+    k = torch.randn(T, Hkv, 128, generator=g).bfloat16()
+    v = torch.randn(T, Hkv, 128, generator=g).bfloat16()
+    cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32)
+    ref = oracle.prefill(q, k, v, cu, causal=causal)
+    qd, kd, vd = q.to(DEV), k.to(DEV), v.to(DEV)
+    out = A.prefill_varlen(qd, kd, vd, cu.to(DEV), max(lens), causal=causal, config=cfg)
+    base = sdpa_prefill_bf16(qd, kd, vd, cu, causal)
+    return out, ref, base
+
+
+# ------------------------------------------------------------------ tcgen05 descriptor self-test
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_umma_selftest(mode):
+    g = torch.Generator().manual_seed(mode)
+    a = torch.randn(128, 128, generator=g).bfloat16().to(DEV)
+    b = torch.randn(16 if mode == 2 else 128, 128, generator=g).bfloat16().to(DEV)
+    d = A.selftest_umma(mode, a, b)
+    af, bf = a.double(), b.double()
+    ref = af @ bf.t() if mode == 0 else (af @ bf if mode == 1 else af.t() @ bf.t())
+    assert (d.double() - ref).abs().max().item() < 1e-3
+
+
+# ------------------------------------------------------------------ golden fixtures (upstream kernel)
+GOLDEN = sorted(glob.glob(str(ROOT / "tests" / "golden" / "*.npz")))
+
+
+def _t(bits, shape=None):
+    return torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16)
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[Path(p).stem for p in GOLDEN])
+def test_golden(path):
+    z = np.load(path)
+    if str(z["kind"]) == "prefill":
+        q, k, v = (_t(z[n]).to(DEV) for n in ("q", "k", "v"))
+        cu = torch.from_numpy(z["cu_seqlens"]).to(DEV)
+        lens = np.diff(z["cu_seqlens"])
+        cfg = pcfg() if (q.shape[1] // k.shape[1]) % 2 == 0 else pcfg(bm=128)
+        out = A.prefill_varlen(q, k, v, cu, int(lens.max()), config=cfg)
+        base = sdpa_prefill_bf16(q, k, v, z["cu_seqlens"], True)
+    else:
+        q, kc, vc = (_t(z[n]).to(DEV) for n in ("q", "k_cache", "v_cache"))
+        bt = torch.from_numpy(z["block_table"]).to(DEV)
+        sl = torch.from_numpy(z["seq_lens"]).to(DEV)
+        out = A.paged_decode(q, kc, vc, bt, sl)
+        base = sdpa_decode_bf16(q, kc, vc, bt, sl)
+    check(Path(path).stem, out, z["out"].astype(np.float64), base)
+
+
+# ------------------------------------------------------------------ prefill
+@pytest.mark.parametrize("lens", [[512], [128], [1], [200], [1, 5, 127, 128, 129, 300], [64, 1000, 3]],
+                         ids=lambda l: "x".join(map(str, l)))
+def test_prefill_causal(lens):
+    out, ref, base = run_prefill(lens)
+    check(f"prefill {lens}", out, ref, base)
+
+
+def test_prefill_noncausal():
+    out, ref, base = run_prefill([200, 64, 129], causal=False)
+    check("prefill noncausal", out, ref, base)
+
+
+@pytest.mark.parametrize("hq,hkv", [(8, 8), (16, 2), (32, 8), (64, 8)])
+def test_prefill_gqa_shapes(hq, hkv):
+    cfg = pcfg(bm=128) if (hq // hkv) % 2 else pcfg()
+    out, ref, base = run_prefill([300, 17], Hq=hq, Hkv=hkv, cfg=cfg)
+    check(f"prefill gqa {hq}/{hkv}", out, ref, base)
+
+
+VARIANTS = [(bm, bn, ns) for bm in (128, 256) for bn in (64, 128) for ns in (2, 3, 4) if not (bm == 256 and bn == 128
+                                                                                               and ns == 4)]
+
+
+@pytest.mark.parametrize("bm,bn,ns", VARIANTS)
+def test_prefill_every_compiled_variant(bm, bn, ns):
+    out, ref, base = run_prefill([300, 77, 129], cfg=pcfg(bm, bn, ns))
+    check(f"prefill variant {bm}/{bn}/{ns}", out, ref, base)
+
+
+def test_prefill_lse():
+    lens = [100, 257]
+    g = torch.Generator().manual_seed(3)
+    T = sum(lens)
+    q, k, v = (torch.randn(T, h, 128, generator=g).bfloat16() for h in (8, 2, 2))
+    cu = torch.tensor([0, 100, 357], dtype=torch.int32)
+    ref, ref_lse = oracle.prefill(q, k, v, cu, with_lse=True)
+    out, lse = A.prefill_varlen(q.to(DEV), k.to(DEV), v.to(DEV), cu.to(DEV), 257, return_lse=True)
+    assert np.abs(lse.cpu().numpy() - ref_lse).max() < 2e-3
+
+
+def test_prefill_c1_full():
+    x = W.make_prefill(W.C1, device="cpu")
+    ref = oracle.prefill(x.q, x.k, x.v, x.cu_seqlens)
+    qd, kd, vd = x.q.to(DEV), x.k.to(DEV), x.v.to(DEV)
+    out = A.prefill_varlen(qd, kd, vd, x.cu_seqlens.to(DEV), x.max_seqlen)
+    check("C1 full", out, ref, sdpa_prefill_bf16(qd, kd, vd, x.cu_seqlens, True))
+
+
+def test_prefill_c3_full_size_subset():
+    """Run all of C3 (16 seqs, 33430 tokens) on the GPU; check the shortest, a middle and the
+    longest sequence on kv heads {0, 7} (their 8 q heads) against the oracle."""
+    x = W.make_prefill(W.C3, device="cpu")
+    out = A.prefill_varlen(x.q.to(DEV), x.k.to(DEV), x.v.to(DEV), x.cu_seqlens.to(DEV), x.max_seqlen).cpu()
+    cu = x.cu_seqlens.tolist()
+    for s in (0, 8, 15):
+        a, b = cu[s], cu[s + 1]
+        for kvh in (0, 7):
+            hs = slice(kvh * 4, kvh * 4 + 4)
+            qq, kk, vv = x.q[a:b, hs].contiguous(), x.k[a:b, kvh:kvh + 1].contiguous(), x.v[a:b, kvh:kvh + 1].contiguous()
+            cu1 = torch.tensor([0, b - a], dtype=torch.int32)
+            ref = oracle.prefill(qq, kk, vv, cu1)
+            base = sdpa_prefill_bf16(qq.to(DEV), kk.to(DEV), vv.to(DEV), cu1, True)
+            check(f"C3 seq{s} (L={b - a}) kvh{kvh}", out[a:b, hs], ref, base)
+
+
+# ------------------------------------------------------------------ decode
+def run_decode(lens, Hq=32, Hkv=8, bs=16, cfg=None, seed=0):
+    shape = dict(W.C2, batch_size=len(lens), seq_len=max(lens), num_q_heads=Hq, num_kv_heads=Hkv, block_size=bs,
+                 seed=seed)
+    d = W.make_decode(shape, device="cpu", lens=lens, extra_blocks=3)
+    ref = oracle.decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)
+    args = [t.to(DEV) for t in (d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)]
+    out = A.paged_decode(*args, config=cfg)
+    return out, ref, sdpa_decode_bf16(*args)
+
+
+@pytest.mark.parametrize("lens", [[1], [128], [4096, 4096], [1, 15, 16, 17, 127, 128, 129, 1000]],
+                         ids=lambda l: "x".join(map(str, l)))
+@pytest.mark.parametrize("splits", [1, 4, 0])
+def test_decode_ragged(lens, splits):
+    out, ref, base = run_decode(lens, cfg=dcfg(splits))
+    check(f"decode {lens} splits={splits}", out, ref, base)
+
+
+@pytest.mark.parametrize("bs", [8, 16, 32, 64, 128])
+def test_decode_block_sizes(bs):
+    out, ref, base = run_decode([700, 3000, 5], bs=bs)
+    check(f"decode bs={bs}", out, ref, base)
+
+
+@pytest.mark.parametrize("hq,hkv", [(8, 8), (32, 8), (64, 8), (16, 1)])
+def test_decode_gqa(hq, hkv):
+    out, ref, base = run_decode([700, 130], Hq=hq, Hkv=hkv)
+    check(f"decode gqa {hq}/{hkv}", out, ref, base)
+
+
+@pytest.mark.parametrize("ns", [2, 3, 4, 5, 6])
+def test_decode_every_stage_count(ns):
+    out, ref, base = run_decode([1000, 333], cfg=dcfg(2, ns))
+    check(f"decode stages={ns}", out, ref, base)
+
+
+def test_decode_c2_full_size():
+    """C2 in full on the GPU; 4 sequences vs the oracle; split-count invariance on all 64."""
+    d = W.make_decode(W.C2, device="cpu")
+    args = [t.to(DEV) for t in (d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)]
+    outs = {s: A.paged_decode(*args, config=dcfg(s)).float() for s in (1, 2, 8, 0)}
+    for s in (2, 8, 0):
+        assert (outs[s] - outs[1]).abs().max().item() < 2e-2
+    sub = [0, 21, 42, 63]
+    bt = d.block_table[sub]
+    ref = oracle.decode(d.q[sub], d.k_cache, d.v_cache, bt, d.seq_lens[sub])
+    base = sdpa_decode_bf16(args[0][sub], args[1], args[2], args[3][sub], args[4][sub])
+    check("C2 full (4 seqs checked)", outs[0][sub], ref, base)
+
+
+def test_decode_c4_shard_subset():
+    """C4 geometry (64q/8kv, ctx 32k) on a 2-sequence shard vs the oracle."""
+    shape = dict(W.C4, batch_size=2)
+    d = W.make_decode(shape, device="cpu")
+    args = [t.to(DEV) for t in (d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)]
+    out = A.paged_decode(*args)
+    ref = oracle.decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)
+    check("C4 shard (2 x 32k)", out, ref, sdpa_decode_bf16(*args))
+
+
+def test_decode_page_permutation_is_bit_exact():
+    d = W.make_decode(dict(W.C2, batch_size=8, seq_len=1000), device="cuda", extra_blocks=16)
+    a = A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)
+    p = torch.randperm(d.k_cache.shape[0], generator=torch.Generator().manual_seed(1)).to(DEV)
+    inv = torch.empty_like(p)
+    inv[p] = torch.arange(len(p), device=DEV)
+    b = A.paged_decode(d.q, d.k_cache[p].contiguous(), d.v_cache[p].contiguous(),
+                       inv[d.block_table.long()].to(torch.int32), d.seq_lens)
+    assert torch.equal(a, b)
+
+
+def test_combine_kernel():
+    rows, S = 37, 5
+    g = torch.Generator().manual_seed(0)
+    po = torch.randn(rows, S, 128, generator=g)
+    m = torch.randn(rows, S, generator=g) * 4
+    m[0, 1:] = -float("inf")
+    l = torch.rand(rows, S, generator=g) + 0.5
+    l[0, 1:] = 0
+    ml = torch.stack([m, l], -1)
+    out = torch.empty(rows, 128, dtype=torch.bfloat16, device=DEV)
+    A.combine(po.to(DEV), ml.contiguous().to(DEV), out)
+    w = torch.exp2(m - m.max(1, keepdim=True).values)
+    ref = (w[..., None] * po).sum(1) / (w * l).sum(1, keepdim=True)
+    assert (out.float().cpu() - ref).abs().max().item() < 2e-2
+
+
+def test_cache_append_bit_exact():
+    NB, bs, Hkv, N = 40, 16, 8, 50
+    g = torch.Generator().manual_seed(0)
+    kc = torch.randn(NB, bs, Hkv, 128, generator=g).bfloat16().to(DEV)
+    vc = torch.randn(NB, bs, Hkv, 128, generator=g).bfloat16().to(DEV)
+    nk = torch.randn(N, Hkv, 128, generator=g).bfloat16().to(DEV)
+    nv = torch.randn(N, Hkv, 128, generator=g).bfloat16().to(DEV)
+    slots = torch.randperm(NB * bs, generator=g)[:N].to(DEV)
+    slots[3] = -1
+    rk, rv = kc.clone().view(-1, Hkv, 128), vc.clone().view(-1, Hkv, 128)
+    keep = slots >= 0
+    rk[slots[keep]] = nk[keep]
+    rv[slots[keep]] = nv[keep]
+    A.cache_append(nk, nv, kc, vc, slots)
+    assert torch.equal(kc.view(-1, Hkv, 128), rk) and torch.equal(vc.view(-1, Hkv, 128), rv)
+
+
+def test_append_then_decode_equals_oracle():
+    """Serving step: append the new token's K/V into its page, then decode (the §8(f) row 2 path)."""
+    lens = [33, 300]
+    d = W.make_decode(dict(W.C2, batch_size=2, seq_len=300), device="cpu", lens=lens, extra_blocks=2)
+    kc, vc = d.k_cache.clone(), d.v_cache.clone()
+    g = torch.Generator().manual_seed(5)
+    nk, nv = (torch.randn(2, 8, 128, generator=g).bfloat16() for _ in range(2))
+    bs = 16
+    slots = torch.tensor([int(d.block_table[b, (lens[b] - 1) // bs]) * bs + (lens[b] - 1) % bs for b in range(2)])
+    kc.view(-1, 8, 128)[slots] = nk
+    vc.view(-1, 8, 128)[slots] = nv
+    ref = oracle.decode(d.q, kc, vc, d.block_table, d.seq_lens)
+    kd, vd = d.k_cache.to(DEV), d.v_cache.to(DEV)
+    A.cache_append(nk.to(DEV), nv.to(DEV), kd, vd, slots.to(DEV))
+    out = A.paged_decode(d.q.to(DEV), kd, vd, d.block_table.to(DEV), d.seq_lens.to(DEV))
+    base = sdpa_decode_bf16(d.q.to(DEV), kd, vd, d.block_table.to(DEV), d.seq_lens.to(DEV))
+    check("append+decode", out, ref, base)
+
+
+# ------------------------------------------------------------------ runner on the GPU
+def test_runner_b200_backend_end_to_end():
+    env = dict(os.environ, PYTHONPATH=str(ROOT))
+    p = subprocess.Popen([sys.executable, "-m", "paper_2505_03780_b200.runner", "--binding",
+                          str(ROOT / "paper_2505_03780_b200/spaces/prefill.binding.json"), "--protocol", "1"],
+                         stdin=subprocess.PIPE, stdout=subprocess.PIPE, text=True, env=env, cwd=ROOT)
+
+    def ask(m):
+        p.stdin.write(json.dumps(m) + "\n")
+        p.stdin.flush()
+        return json.loads(p.stdout.readline())
+
+    hello = ask({"type": "hello", "protocol": 1})
+    assert "B200" in hello["fingerprint"]["device_name"] and "graph-timing" in hello["capabilities"]
+    shape = dict(W.C1)
+    ok = ask({"type": "evaluate", "config": pcfg(), "shape": shape, "warmups": 2, "reps": 5})
+    assert ok["status"] == "ok" and len(ok["latencies_ms"]) == 5 and ok["compile_ms"] > 0
+    bad = ask({"type": "evaluate", "config": pcfg(bm=64, bn=64), "shape": shape, "warmups": 1, "reps": 2})
+    assert bad["status"] == "invalid" and "BLOCK_M" in bad["reason"]
+    p.stdin.write(json.dumps({"type": "shutdown"}) + "\n")
+    p.stdin.flush()
+    assert p.wait(timeout=30) == 0
