@@ -221,3 +221,62 @@ def selftest_umma(mode: int, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
 
 def default_scale(head_dim: int) -> float:
     return 1.0 / math.sqrt(head_dim)
+
+
+class DecodePlan:
+    """Plan/run split for serving loops and CUDA-graph capture: validates once, pins the
+    params struct and workspace, then ``run()`` is a single C-ABI call (K2 [+K3])."""
+
+    def __init__(self, q, k_cache, v_cache, block_table, seq_lens, out=None, max_seq_len=None, config=None,
+                 softmax_scale=None):
+        self.lib = _native.load()
+        for t, n in ((q, "q"), (k_cache, "k_cache"), (v_cache, "v_cache")):
+            _check(t, n)
+        _check(block_table, "block_table", dtype=torch.int32, ndim=2)
+        _check(seq_lens, "seq_lens", dtype=torch.int32, ndim=1)
+        self.max_seq_len = int(max_seq_len if max_seq_len is not None else block_table.shape[1] * k_cache.shape[1])
+        self.out = torch.empty_like(q) if out is None else out
+        self.config = dict(config or default_decode_config(
+            batch_size=q.shape[0], seq_len=self.max_seq_len, num_q_heads=q.shape[1], num_kv_heads=k_cache.shape[2],
+            head_dim=q.shape[2], block_size=k_cache.shape[1]))
+        self.var = decode_variant(self.config)
+        self.p = _decode_params(q, k_cache, v_cache, block_table, seq_lens, self.out, self.max_seq_len, softmax_scale)
+        nbytes = self.lib.b200attn_decode_workspace_size(self.p, self.var)
+        self.ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=q.device) if nbytes else None
+        if self.ws is not None:
+            self.p.workspace, self.p.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
+        self.num_splits = int(self.lib.b200attn_decode_num_splits(self.p, self.var))
+        self.device = q.device
+
+    def kernels_per_run(self) -> int:
+        return 2 if self.num_splits > 1 else 1
+
+    def run(self, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        _native.check(self.lib.b200attn_decode(self.p, self.var, s))
+        return self.out
+
+    def run_partial(self, stream=None):
+        """K2 only (the dominant kernel), for roofline timing."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        _native.check(self.lib.b200attn_decode_partial(self.p, self.var, s))
+
+
+class PrefillPlan:
+    def __init__(self, q, k, v, cu_seqlens, max_seqlen, out=None, causal=True, config=None, softmax_scale=None):
+        self.lib = _native.load()
+        for t, n in ((q, "q"), (k, "k"), (v, "v")):
+            _check(t, n, ndim=3)
+        _check(cu_seqlens, "cu_seqlens", dtype=torch.int32, ndim=1)
+        self.out = torch.empty_like(q) if out is None else out
+        self.config = dict(config or default_prefill_config(
+            num_seqs=cu_seqlens.numel() - 1, total_tokens=q.shape[0], max_seqlen=int(max_seqlen),
+            num_q_heads=q.shape[1], num_kv_heads=k.shape[1], head_dim=q.shape[2], causal=causal))
+        self.var = prefill_variant(self.config)
+        self.p = _prefill_params(q, k, v, self.out, cu_seqlens, max_seqlen, softmax_scale, causal, None)
+        self.device = q.device
+
+    def run(self, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        _native.check(self.lib.b200attn_prefill(self.p, self.var, s))
+        return self.out

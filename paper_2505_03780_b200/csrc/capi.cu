@@ -186,10 +186,10 @@ int check_prefill(const b200attn_prefill_params* p, const b200attn_prefill_varia
 }
 
 // ------------------------------------------------------------------ decode variants
-using DecodeLauncher = int (*)(const b200attn_decode_params*, int splits, int tps, cudaStream_t);
+using DecodeLauncher = int (*)(const b200attn_decode_params*, int splits, int tps, bool combine, cudaStream_t);
 
 template <int NS>
-int launch_decode(const b200attn_decode_params* p, int splits, int tps, cudaStream_t stream) {
+int launch_decode(const b200attn_decode_params* p, int splits, int tps, bool combine, cudaStream_t stream) {
   using C = b200::DecodeCfg<NS>;
   auto kern = b200::decode_split_kernel<NS>;
   static bool attr_done = false;
@@ -230,7 +230,7 @@ int launch_decode(const b200attn_decode_params* p, int splits, int tps, cudaStre
   kern<<<grid, C::NTHREADS, C::SMEM_BYTES, stream>>>(mq, mk, mv, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "decode launch");
-  if (splits > 1) {
+  if (splits > 1 && combine) {
     b200::decode_combine_kernel<<<(unsigned)rows, 128, 0, stream>>>(a.part_o, a.part_ml,
                                                                     reinterpret_cast<__nv_bfloat16*>(p->o), splits);
     e = cudaGetLastError();
@@ -372,7 +372,8 @@ size_t b200attn_decode_workspace_size(const b200attn_decode_params* p, const b20
   return rows * s * (128 + 2) * sizeof(float);
 }
 
-int b200attn_decode(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream) {
+static int decode_impl(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream,
+                       bool combine) {
   const DecodeEntry* e;
   g_err[0] = 0;
   int rc = check_decode(p, v, &e);
@@ -386,7 +387,15 @@ int b200attn_decode(const b200attn_decode_params* p, const b200attn_decode_varia
     if (!p->workspace || p->workspace_bytes < need)
       return fail(B200ATTN_BAD_ARGS, "workspace %zu B < %zu B needed for %d splits", p->workspace_bytes, need, s);
   }
-  return e->fn(p, s, t, reinterpret_cast<cudaStream_t>(stream));
+  return e->fn(p, s, t, combine, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int b200attn_decode(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream) {
+  return decode_impl(p, v, stream, true);
+}
+
+int b200attn_decode_partial(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream) {
+  return decode_impl(p, v, stream, false);
 }
 
 int b200attn_combine(const float* part_o, const float* part_ml, void* o, int32_t rows, int32_t num_splits,
