@@ -249,7 +249,7 @@ class DecodePlan:
         self.device = q.device
 
     def kernels_per_run(self) -> int:
-        return 2 if self.num_splits > 1 else 1
+        return 2 if (self.num_splits > 1 or int(self.config["TILE_N"]) == 16) else 1
 
     def run(self, stream=None):
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream

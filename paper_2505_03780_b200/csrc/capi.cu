@@ -14,6 +14,7 @@
 #include <mutex>
 
 #include "../../include/b200attn.h"
+#include "decode_flat_sm100.cuh"
 #include "decode_sm100.cuh"
 #include "prefill_sm100.cuh"
 #include "selftest_sm100.cuh"
@@ -248,6 +249,112 @@ struct DecodeEntry {
 const DecodeEntry kDecode[] = {DF(2), DF(3), DF(4), DF(5), DF(6)};
 #undef DF
 
+
+// ---- K2' flat partition (TILE_N = 16: one page of all 8 kv heads per MMA tile)
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
+  }
+  return n;
+}
+
+size_t flat_workspace_bytes(const b200attn_decode_params* p) {
+  const size_t slots = (size_t)num_sms() + p->batch;
+  return slots * p->num_q_heads * (128 + 2) * sizeof(float) + ((size_t)p->batch + 1) * sizeof(int32_t);
+}
+
+using FlatLauncher = int (*)(const b200attn_decode_params*, bool combine, cudaStream_t);
+
+template <int G, int NS>
+int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stream) {
+  using C = b200::FlatCfg<G, NS>;
+  auto kern = b200::decode_flat_kernel<G, NS>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode_flat)");
+    attr_done = true;
+  }
+  const int D = 128;
+  CUtensorMap mq, mk, mv;
+  int rc;
+  if ((rc = make_map_3d(&mq, p->q, D, p->num_q_heads, p->batch, D * 2ull, (uint64_t)p->num_q_heads * D * 2,
+                        C::NQ, 1)))
+    return rc;
+  // head-major view of the page pool: dims {d, token, head}, strides {Hkv*D*2, D*2} (transposed)
+  const uint64_t tokens = (uint64_t)p->num_blocks * p->block_size;
+  if ((rc = make_map_3d(&mk, p->k_cache, D, tokens, 8, 8ull * D * 2, D * 2ull, C::TT, 8))) return rc;
+  if ((rc = make_map_3d(&mv, p->v_cache, D, tokens, 8, 8ull * D * 2, D * 2ull, C::TT, 8))) return rc;
+  const int ctas = num_sms();
+  const size_t slots = (size_t)ctas + p->batch;
+  b200::FlatDecodeArgs a;
+  a.block_table = p->block_table;
+  a.seq_lens = p->seq_lens;
+  a.o = reinterpret_cast<__nv_bfloat16*>(p->o);
+  a.part_o = reinterpret_cast<float*>(p->workspace);
+  a.part_ml = a.part_o + slots * p->num_q_heads * 128;
+  a.cu_tiles_out = reinterpret_cast<int32_t*>(a.part_ml + slots * p->num_q_heads * 2);
+  a.batch = p->batch;
+  a.block_size = p->block_size;
+  a.max_blocks = p->max_blocks_per_seq;
+  const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / sqrtf((float)p->head_dim);
+  a.scale_log2 = scale * 1.4426950408889634f;
+  kern<<<ctas, C::NTHREADS, C::SMEM_BYTES, stream>>>(mq, mk, mv, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "decode_flat launch");
+  if (combine) {
+    b200::flat_combine_kernel<C::NQ><<<dim3(p->batch, C::NQ), 128, 0, stream>>>(
+        a.part_o, a.part_ml, a.cu_tiles_out, p->batch, ctas, reinterpret_cast<__nv_bfloat16*>(p->o));
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "flat combine launch");
+  }
+  return B200ATTN_OK;
+}
+
+struct FlatEntry {
+  int g, ns;
+  FlatLauncher fn;
+  int smem;
+};
+#define FF(G, NS) {G, NS, &launch_flat<G, NS>, b200::FlatCfg<G, NS>::SMEM_BYTES}
+const FlatEntry kFlat[] = {FF(1, 3), FF(1, 4), FF(1, 5), FF(1, 6), FF(2, 3), FF(2, 4), FF(2, 5), FF(2, 6),
+                           FF(4, 3), FF(4, 4), FF(4, 5), FF(8, 3), FF(8, 4)};
+#undef FF
+
+int check_flat(const b200attn_decode_params* p, const b200attn_decode_variant* v, const FlatEntry** out) {
+  if (v->num_splits != 0)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG,
+                "num_splits=%d: TILE_N=16 uses the flat stream partition (one CTA per SM); num_splits must be 0",
+                v->num_splits);
+  if (p->num_kv_heads != 8)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16 packs 8 kv heads x 16 tokens per tile; num_kv_heads=%d",
+                p->num_kv_heads);
+  const int G = p->num_q_heads / p->num_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16 compiled for GQA groups 1/2/4/8, got %d", G);
+  if (p->block_size < 16)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16 needs block_size >= 16, got %d", p->block_size);
+  if (p->batch > b200::FlatCfg<1, 3>::MAXB)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16 supports batch <= %d", b200::FlatCfg<1, 3>::MAXB);
+  const FlatEntry* e = nullptr;
+  for (const auto& x : kFlat)
+    if (x.g == G && x.ns == v->num_stages) e = &x;
+  if (!e) {
+    const int np = 8 * G < 16 ? 16 : 8 * G;
+    const int est = v->num_stages * 32768 + 4 * np * 256 + 4096 + 1024;
+    if (est > kMaxSmem)
+      return fail(B200ATTN_SMEM_OVERFLOW, "TILE_N=16 num_stages=%d with %d q heads needs ~%d B smem > %d",
+                  v->num_stages, p->num_q_heads, est, kMaxSmem);
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16: no compiled variant for num_stages=%d", v->num_stages);
+  }
+  if (e->smem > kMaxSmem) return fail(B200ATTN_SMEM_OVERFLOW, "decode_flat smem %d B", e->smem);
+  *out = e;
+  return B200ATTN_OK;
+}
+
 int decode_ctas_per_sm(int smem) {
   const int per_sm = 233472;  // 228 KB per SM
   int n = per_sm / (smem + 1024);
@@ -274,9 +381,26 @@ void resolve_splits(const b200attn_decode_params* p, const b200attn_decode_varia
   *tps = t;
 }
 
+int check_decode_common(const b200attn_decode_params* p) {
+  if (p->head_dim != 128) return fail(B200ATTN_UNSUPPORTED_CONFIG, "head_dim=%d (compiled for 128)", p->head_dim);
+  if (p->num_kv_heads <= 0 || p->num_q_heads % p->num_kv_heads)
+    return fail(B200ATTN_BAD_ARGS, "num_q_heads=%d not a multiple of num_kv_heads=%d", p->num_q_heads,
+                p->num_kv_heads);
+  const int bs = p->block_size;
+  if (bs < 8 || bs > 128 || (bs & (bs - 1)))
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "block_size=%d: pages must be a power of two in [8,128]", bs);
+  if (p->batch <= 0 || p->batch > 65535 || p->num_blocks <= 0 || p->max_blocks_per_seq <= 0)
+    return fail(B200ATTN_BAD_ARGS, "batch=%d num_blocks=%d max_blocks_per_seq=%d", p->batch, p->num_blocks,
+                p->max_blocks_per_seq);
+  if (p->max_seq_len > p->max_blocks_per_seq * bs)
+    return fail(B200ATTN_BAD_ARGS, "max_seq_len=%d exceeds block_table capacity %d", p->max_seq_len,
+                p->max_blocks_per_seq * bs);
+  return B200ATTN_OK;
+}
+
 int check_decode(const b200attn_decode_params* p, const b200attn_decode_variant* v, const DecodeEntry** out) {
   if (!p || !v) return fail(B200ATTN_BAD_ARGS, "null params/variant");
-  if (v->tile_n != 128) return fail(B200ATTN_UNSUPPORTED_CONFIG, "tile_n=%d (compiled for 128)", v->tile_n);
+  if (v->tile_n != 128) return fail(B200ATTN_UNSUPPORTED_CONFIG, "tile_n=%d (compiled: 16, 128)", v->tile_n);
   const DecodeEntry* e = nullptr;
   for (const auto& x : kDecode)
     if (x.ns == v->num_stages) e = &x;
@@ -300,6 +424,19 @@ int check_decode(const b200attn_decode_params* p, const b200attn_decode_variant*
                 p->max_blocks_per_seq * bs);
   *out = e;
   return B200ATTN_OK;
+}
+
+struct DecodeChoice {
+  const DecodeEntry* split = nullptr;
+  const FlatEntry* flat = nullptr;
+};
+
+int resolve_decode(const b200attn_decode_params* p, const b200attn_decode_variant* v, DecodeChoice* c) {
+  if (!p || !v) return fail(B200ATTN_BAD_ARGS, "null params/variant");
+  int rc = check_decode_common(p);
+  if (rc) return rc;
+  if (v->tile_n == 16) return check_flat(p, v, &c->flat);
+  return check_decode(p, v, &c->split);
 }
 
 }  // namespace
@@ -347,26 +484,28 @@ int b200attn_prefill(const b200attn_prefill_params* p, const b200attn_prefill_va
 
 int b200attn_decode_supported(const b200attn_decode_params* p, const b200attn_decode_variant* v, char* reason,
                               size_t n) {
-  const DecodeEntry* e;
+  DecodeChoice c;
   g_err[0] = 0;
-  int rc = check_decode(p, v, &e);
+  int rc = resolve_decode(p, v, &c);
   copy_reason(reason, n);
   return rc;
 }
 
 int b200attn_decode_num_splits(const b200attn_decode_params* p, const b200attn_decode_variant* v) {
-  const DecodeEntry* e;
-  if (check_decode(p, v, &e)) return -1;
+  DecodeChoice c;
+  if (resolve_decode(p, v, &c)) return -1;
+  if (c.flat) return num_sms();  // stream partition: one range per CTA
   int s, t;
-  resolve_splits(p, v, e->smem, &s, &t);
+  resolve_splits(p, v, c.split->smem, &s, &t);
   return s;
 }
 
 size_t b200attn_decode_workspace_size(const b200attn_decode_params* p, const b200attn_decode_variant* v) {
-  const DecodeEntry* e;
-  if (check_decode(p, v, &e)) return 0;
+  DecodeChoice c;
+  if (resolve_decode(p, v, &c)) return 0;
+  if (c.flat) return flat_workspace_bytes(p);
   int s, t;
-  resolve_splits(p, v, e->smem, &s, &t);
+  resolve_splits(p, v, c.split->smem, &s, &t);
   if (s <= 1) return 0;
   const size_t rows = (size_t)p->batch * p->num_q_heads;
   return rows * s * (128 + 2) * sizeof(float);
@@ -374,20 +513,26 @@ size_t b200attn_decode_workspace_size(const b200attn_decode_params* p, const b20
 
 static int decode_impl(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream,
                        bool combine) {
-  const DecodeEntry* e;
+  DecodeChoice c;
   g_err[0] = 0;
-  int rc = check_decode(p, v, &e);
+  int rc = resolve_decode(p, v, &c);
   if (rc) return rc;
   if (!p->q || !p->k_cache || !p->v_cache || !p->block_table || !p->seq_lens || !p->o)
     return fail(B200ATTN_BAD_ARGS, "null tensor pointer");
+  if (c.flat) {
+    const size_t need = flat_workspace_bytes(p);
+    if (!p->workspace || p->workspace_bytes < need)
+      return fail(B200ATTN_BAD_ARGS, "workspace %zu B < %zu B needed (flat partition)", p->workspace_bytes, need);
+    return c.flat->fn(p, combine, reinterpret_cast<cudaStream_t>(stream));
+  }
   int s, t;
-  resolve_splits(p, v, e->smem, &s, &t);
+  resolve_splits(p, v, c.split->smem, &s, &t);
   if (s > 1) {
     const size_t need = (size_t)p->batch * p->num_q_heads * s * (128 + 2) * sizeof(float);
     if (!p->workspace || p->workspace_bytes < need)
       return fail(B200ATTN_BAD_ARGS, "workspace %zu B < %zu B needed for %d splits", p->workspace_bytes, need, s);
   }
-  return e->fn(p, s, t, combine, reinterpret_cast<cudaStream_t>(stream));
+  return c.split->fn(p, s, t, combine, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int b200attn_decode(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream) {

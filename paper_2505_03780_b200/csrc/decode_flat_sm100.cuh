@@ -1,0 +1,411 @@
+// decode_flat_sm100.cuh — K2': paged-KV decode, flat (stream-K style) partition, all KV heads
+// per CTA, sm_100a.   Selected by TILE_N = 16 (tokens per MMA tile).
+//
+// Why: a page of the vLLM cache [num_blocks, bs, Hkv=8, 128] holds 16 tokens x 8 heads = 32 KB
+// contiguous.  K2 (decode_sm100.cuh) gathers it per kv head as 2-KB strided boxes; here one
+// TMA box {64 d, 16 tokens, 8 heads} per 64-column half moves the whole page, and the MMA M
+// dimension is the page's 128 (head, token) rows.  The tensor map is head-major (strides
+// {2048 B token, 256 B head} — transposed) so smem row r = head*16 + token: every warp owns
+// two heads, the per-head max over the tile is a 16-lane shuffle and nothing crosses warps.
+//
+//   S^T[(h,t), qh] = K_page[(h,t), :] . Q[qh, :]^T            M=128 rows, N = Hq (pad 16)
+//   O^T[d, qh]    += V_page^T[d, (h,t)] . P^T[(h,t), qh]       P^T block-diagonal: entries with
+//                                                              qh / G != h are never written
+//                                                              (zeroed once per CTA)
+// Work: the tiles of all sequences are laid end to end (cu_tiles) and cut into gridDim.x equal
+// contiguous ranges — one persistent CTA per SM, perfectly balanced for any length mix.  A
+// range may cover several sequences and parts of sequences; each (CTA, sequence) piece is a
+// segment: complete sequences are normalised and written by the CTA, pieces go to partial slot
+// (cta + seq) and K3' (flat_combine_kernel) merges them.
+#pragma once
+#include "sm100_common.cuh"
+
+namespace b200 {
+
+struct FlatDecodeArgs {
+  const int32_t* block_table;  // [B, max_blocks]
+  const int32_t* seq_lens;     // [B]
+  __nv_bfloat16* o;            // [B, Hq, 128]
+  float* part_o;               // [(ctas + B), Hq, 128]
+  float* part_ml;              // [(ctas + B), Hq, 2]  (max in log2 units, sum)
+  int32_t* cu_tiles_out;       // [B + 1] (written by CTA 0 for the combine)
+  int32_t batch;
+  int32_t block_size;
+  int32_t max_blocks;
+  float scale_log2;
+};
+
+template <int G, int NSTAGE>
+struct FlatCfg {
+  static constexpr int D = 128, HKV = 8, TT = 16, ROWS = 128;
+  static constexpr int NQ = 8 * G;
+  static constexpr int NP = NQ < 16 ? 16 : NQ;  // MMA N
+  static constexpr int NTHREADS = 192, TMA_WARP = 4, MMA_WARP = 5;
+  static constexpr int SLOT = ROWS * D * 2, HALF = ROWS * 128;
+  static constexpr int QB = NP * 256, QHALF = NP * 128;
+  static constexpr int PB = NP * 256, PHALF = NP * 128;
+  static constexpr int MAXB = 1024;
+  static constexpr int OFF_KV = 0;
+  static constexpr int OFF_Q = OFF_KV + NSTAGE * SLOT;
+  static constexpr int OFF_P = OFF_Q + 2 * QB;
+  static constexpr int OFF_ALPHA = OFF_P + 2 * PB;     // [3][NP] f32
+  static constexpr int OFF_ML = OFF_ALPHA + 3 * NP * 4;  // [2][NP] f32
+  static constexpr int OFF_CU = OFF_ML + 2 * NP * 4;     // [MAXB + 1] i32
+  static constexpr int OFF_BAR = (OFF_CU + (MAXB + 1) * 4 + 7) & ~7;
+  static constexpr int NUM_BARS = 4 + 2 * NSTAGE + 8;
+  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  static constexpr uint32_t TMEM_COLS = (4 * NP <= 64) ? 64 : (4 * NP <= 128 ? 128 : 256);
+  __host__ __device__ static constexpr uint32_t S_COL(int i) { return (i & 1) * NP; }
+  __host__ __device__ static constexpr uint32_t O_COL(int i) { return 2 * NP + (i & 1) * NP; }
+};
+
+__device__ __forceinline__ int flat_cta_of(int t, int ctas, int ntiles) {
+  return static_cast<int>(((static_cast<long long>(t) + 1) * ctas - 1) / ntiles);
+}
+
+template <int G, int NSTAGE>
+__global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
+    decode_flat_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
+                       const __grid_constant__ CUtensorMap tmap_v, const FlatDecodeArgs args) {
+  using C = FlatCfg<G, NSTAGE>;
+  constexpr int NQ = C::NQ, NP = C::NP, D = C::D;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sKV = smem + C::OFF_KV;
+  uint8_t* sQ = smem + C::OFF_Q;
+  uint8_t* sP = smem + C::OFF_P;
+  float* alpha_s = reinterpret_cast<float*>(smem + C::OFF_ALPHA);
+  float* ml_s = reinterpret_cast<float*>(smem + C::OFF_ML);
+  int32_t* cu = reinterpret_cast<int32_t*>(smem + C::OFF_CU);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars;           // [2]
+  uint64_t* q_empty = bars + 2;      // [2]
+  uint64_t* kv_full = bars + 4;      // [NSTAGE]
+  uint64_t* kv_empty = kv_full + NSTAGE;
+  uint64_t* s_full = kv_empty + NSTAGE;  // [2]
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_full = p_full + 2;
+  uint64_t* o_empty = o_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS);
+  const int warp = warp_id(), lane = lane_id();
+  const int B = args.batch;
+
+  // ---- tiles per sequence -> cu (exclusive prefix), one warp
+  if (warp == 0) {
+    int carry = 0;
+    if (lane == 0) cu[0] = 0;
+    for (int base = 0; base < B; base += 32) {
+      const int b = base + lane;
+      int v = b < B ? (args.seq_lens[b] + C::TT - 1) / C::TT : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, v, off);
+        if (lane >= off) v += n;
+      }
+      if (b < B) cu[b + 1] = carry + v;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  // zero Q (padded rows) and P^T (block-diagonal zeros) once
+  for (int i = threadIdx.x; i < (2 * C::QB + 2 * C::PB) / 16; i += C::NTHREADS)
+    reinterpret_cast<uint4*>(sQ)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 32) {
+    mbar_init(&q_full[0], 1);
+    mbar_init(&q_full[1], 1);
+    mbar_init(&q_empty[0], 1);
+    mbar_init(&q_empty[1], 1);
+    for (int i = 0; i < NSTAGE; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  const int ntiles = cu[B];
+  const int T0 = static_cast<int>(static_cast<long long>(blockIdx.x) * ntiles / gridDim.x);
+  const int T1 = static_cast<int>((static_cast<long long>(blockIdx.x) + 1) * ntiles / gridDim.x);
+  if (blockIdx.x == 0)
+    for (int b = threadIdx.x; b <= B; b += C::NTHREADS) args.cu_tiles_out[b] = cu[b];
+  if (T0 >= T1) return;  // more CTAs than tiles (uniform per CTA)
+  // first sequence with tiles beyond T0
+  int b_first;
+  {
+    int lo = 0, hi = B - 1;  // smallest b with cu[b+1] > T0
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cu[mid + 1] > T0) hi = mid;
+      else lo = mid + 1;
+    }
+    b_first = lo;
+  }
+
+  if (warp == C::MMA_WARP) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == C::TMA_WARP) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tmap_q);
+      tma_prefetch_desc(&tmap_k);
+      tma_prefetch_desc(&tmap_v);
+    }
+    const uint64_t stream_once = policy_evict_first();
+    const int bs = args.block_size;
+    int it = 0, k = 0, b = b_first;
+    for (int t = T0; t < T1; ++k) {
+      while (cu[b + 1] <= t) ++b;
+      const int seg_end = min(T1, cu[b + 1]);
+      const int tile0 = cu[b];
+      if (lane == 0) {
+        mbar_wait(&q_empty[k & 1], ((k >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[k & 1], 2 * NQ * 128);
+        for (int hf = 0; hf < 2; ++hf)
+          tma_load_3d(sQ + (k & 1) * C::QB + hf * C::QHALF, &tmap_q, &q_full[k & 1], hf * 64, 0, b);
+      }
+      const int32_t* bt = args.block_table + static_cast<size_t>(b) * args.max_blocks;
+      for (int base = t; base < seg_end; base += 32) {
+        const int n = min(32, seg_end - base);
+        int page = 0;
+        if (lane < n) page = __ldg(bt + ((base + lane - tile0) * C::TT) / bs);
+        for (int j = 0; j < n; ++j) {
+          const int pg = __shfl_sync(0xffffffffu, page, j);
+          const int tok = (base + j - tile0) * C::TT;
+          const int row = pg * bs + (tok & (bs - 1));
+          if (lane == 0) {
+#pragma unroll
+            for (int kv = 0; kv < 2; ++kv, ++it) {
+              const int slot = it % NSTAGE;
+              mbar_wait(&kv_empty[slot], ((it / NSTAGE) & 1) ^ 1);
+              mbar_arrive_expect_tx(&kv_full[slot], C::SLOT);
+              uint8_t* dst = sKV + slot * C::SLOT;
+              const CUtensorMap* map = kv ? &tmap_v : &tmap_k;
+              tma_load_3d_hint(dst, map, &kv_full[slot], 0, row, 0, stream_once);
+              tma_load_3d_hint(dst + C::HALF, map, &kv_full[slot], 64, row, 0, stream_once);
+            }
+          }
+        }
+      }
+      t = seg_end;
+    }
+  } else if (warp == C::MMA_WARP) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IDESC_QK = idesc_bf16_f32(C::ROWS, NP, false, false);
+      constexpr uint32_t IDESC_PV = idesc_bf16_f32(D, NP, true, false);
+      const uint32_t kv_base = smem_u32(sKV), q_base = smem_u32(sQ), p_base = smem_u32(sP);
+      auto qk = [&](int i, int qb) {
+        const int idx = 2 * i, slot = idx % NSTAGE;
+        mbar_wait(&kv_full[slot], (idx / NSTAGE) & 1);
+        tc_fence_after();
+        const uint32_t kb = kv_base + slot * C::SLOT, qa = q_base + qb * C::QB;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t da = sdesc_sw128(kb + (kk >> 2) * C::HALF + (kk & 3) * 32, 16, 1024);
+          const uint64_t db = sdesc_sw128(qa + (kk >> 2) * C::QHALF + (kk & 3) * 32, 16, 1024);
+          umma_ss(tmem + C::S_COL(i), da, db, IDESC_QK, kk > 0);
+        }
+        umma_commit(&s_full[i & 1]);
+        umma_commit(&kv_empty[slot]);
+      };
+      auto pv = [&](int i) {
+        const int idx = 2 * i + 1, slot = idx % NSTAGE;
+        mbar_wait(&kv_full[slot], (idx / NSTAGE) & 1);
+        mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+        if (i >= 2) mbar_wait(&o_empty[i & 1], ((i >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t vb = kv_base + slot * C::SLOT, pb = p_base + (i & 1) * C::PB;
+#pragma unroll
+        for (int kk = 0; kk < C::ROWS / 16; ++kk) {
+          const uint64_t da = sdesc_sw128(vb + kk * 16 * 128, C::HALF, 1024);
+          const uint64_t db = sdesc_sw128(pb + (kk >> 2) * C::PHALF + (kk & 3) * 32, 16, 1024);
+          umma_ss(tmem + C::O_COL(i), da, db, IDESC_PV, kk > 0);
+        }
+        umma_commit(&o_full[i & 1]);
+        umma_commit(&kv_empty[slot]);
+      };
+      int i = 0, k = 0, b = b_first;
+      for (int t = T0; t < T1; ++k) {
+        while (cu[b + 1] <= t) ++b;
+        const int seg_end = min(T1, cu[b + 1]);
+        mbar_wait(&q_full[k & 1], (k >> 1) & 1);
+        for (; t < seg_end; ++t, ++i) {
+          qk(i, k & 1);
+          if (t == seg_end - 1) umma_commit(&q_empty[k & 1]);
+          if (i >= 1) pv(i - 1);
+        }
+      }
+      pv(i - 1);
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / fold / epilogue
+    const int row = threadIdx.x;  // S^T row (head*16 + token) and O^T row (d)
+    const int h = row >> 4, t16 = row & 15;
+    const bool upper = (lane >> 4) != 0;
+    const uint32_t lane_base = static_cast<uint32_t>(warp << 5) << 16;
+    const uint32_t col_base = static_cast<uint32_t>(warp * 2 * G);
+    const float sl2 = args.scale_log2;
+    const uint32_t p_base = smem_u32(sP) + (row >> 6) * C::PHALF + (row & 7) * 2;
+    const int rchunk = (row & 63) >> 3;
+
+    float m_run[G], l_part[G], o_acc[NQ];
+    auto fold = [&](int j) {
+      mbar_wait(&o_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t r[NQ];
+      tmem_ld_cols<NQ>(tmem + lane_base + C::O_COL(j), r);
+      const float* al = alpha_s + (j % 3) * NP;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) o_acc[q] = fmaf(o_acc[q], al[q], __uint_as_float(r[q]));
+      tc_fence_before();
+      mbar_arrive(&o_empty[j & 1]);
+    };
+
+    int i = 0, b = b_first;
+    for (int t = T0; t < T1;) {
+      while (cu[b + 1] <= t) ++b;
+      const int seg_end = min(T1, cu[b + 1]);
+      const int tile0 = cu[b];
+      const int len = args.seq_lens[b];
+      const bool complete = (t == tile0) && (seg_end == cu[b + 1]);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        m_run[g] = -INFINITY;
+        l_part[g] = 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) o_acc[q] = 0.f;
+      const int first_i = i;
+      for (; t < seg_end; ++t, ++i) {
+        const int sb = i & 1;
+        mbar_wait(&s_full[sb], (i >> 1) & 1);
+        tc_fence_after();
+        uint32_t sv[2 * G];
+        tmem_ld_cols<2 * G>(tmem + lane_base + C::S_COL(i) + col_base, sv);
+        const int tok = (t - tile0) * C::TT + t16;
+        const bool valid = tok < len;
+        float alpha[G];
+        const uint32_t pb = p_base + sb * C::PB;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float s = __uint_as_float(upper ? sv[G + g] : sv[g]);
+          const float x = valid ? s * sl2 : -INFINITY;
+          float mt = x;
+#pragma unroll
+          for (int off = 1; off < 16; off <<= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
+          const float mn = fmaxf(m_run[g], mt);
+          const float mu = (mn == -INFINITY) ? 0.f : mn;
+          alpha[g] = fast_exp2(m_run[g] - mu);
+          const float p = fast_exp2(x - mu);
+          l_part[g] = fmaf(l_part[g], alpha[g], p);
+          m_run[g] = mn;
+          const int qh = h * G + g;
+          const __nv_bfloat16 pv16 = __float2bfloat16_rn(p);
+          asm volatile("st.shared.b16 [%0], %1;" ::"r"(pb + qh * 128 + ((rchunk ^ (qh & 7)) << 4)),
+                       "h"(*reinterpret_cast<const uint16_t*>(&pv16))
+                       : "memory");
+          if (t16 == 0) alpha_s[(i % 3) * NP + qh] = alpha[g];
+        }
+        if (!valid) {
+          // the page's tail slots past the sequence end hold arbitrary bytes: P = 0 there, but
+          // 0 * NaN would poison O, so zero this row of the V tile before PV reads it
+          const int vidx = 2 * i + 1, vslot = vidx % NSTAGE;
+          mbar_wait(&kv_full[vslot], (vidx / NSTAGE) & 1);
+          uint4* vr = reinterpret_cast<uint4*>(sKV + vslot * C::SLOT + row * 128);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            vr[c] = make_uint4(0, 0, 0, 0);
+            vr[C::HALF / 16 + c] = make_uint4(0, 0, 0, 0);
+          }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&p_full[sb]);
+        named_bar_sync(1, 128);  // alpha_s[i % 3] visible to every fold
+        if (i > first_i) fold(i - 1);
+      }
+      fold(i - 1);
+
+      // ---- segment epilogue
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float l = l_part[g];
+#pragma unroll
+        for (int off = 1; off < 16; off <<= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+        if (t16 == 0) {
+          ml_s[h * G + g] = m_run[g];
+          ml_s[NP + h * G + g] = l;
+        }
+      }
+      named_bar_sync(1, 128);
+      if (complete) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const float l = ml_s[NP + q];
+          args.o[(static_cast<size_t>(b) * NQ + q) * D + row] = __float2bfloat16_rn(l > 0.f ? o_acc[q] / l : 0.f);
+        }
+      } else {
+        const size_t slot = static_cast<size_t>(blockIdx.x) + b;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) args.part_o[(slot * NQ + q) * D + row] = o_acc[q];
+        if (row < NQ) {
+          args.part_ml[(slot * NQ + row) * 2 + 0] = ml_s[row];
+          args.part_ml[(slot * NQ + row) * 2 + 1] = ml_s[NP + row];
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == C::MMA_WARP) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// K3': merge the partial segments of every split sequence (sequences finished inside one CTA
+// were already written by it).
+template <int NQ>
+__global__ void __launch_bounds__(128) flat_combine_kernel(const float* __restrict__ part_o,
+                                                           const float* __restrict__ part_ml,
+                                                           const int32_t* __restrict__ cu, int batch, int ctas,
+                                                           __nv_bfloat16* __restrict__ o) {
+  const int b = blockIdx.x, q = blockIdx.y, d = threadIdx.x;
+  const int ts = cu[b], te = cu[b + 1], n = cu[batch];
+  __nv_bfloat16* out = o + (static_cast<size_t>(b) * NQ + q) * 128 + d;
+  if (ts == te) {
+    *out = __float2bfloat16_rn(0.f);
+    return;
+  }
+  const int c0 = flat_cta_of(ts, ctas, n), c1 = flat_cta_of(te - 1, ctas, n);
+  if (c0 == c1) return;
+  // CTAs whose range is empty (fewer tiles than CTAs) wrote nothing: skip their slots
+  auto owns = [&](int c) {
+    return static_cast<long long>(c) * n / ctas != (static_cast<long long>(c) + 1) * n / ctas;
+  };
+  float M = -INFINITY;
+  for (int c = c0; c <= c1; ++c)
+    if (owns(c)) M = fmaxf(M, part_ml[((static_cast<size_t>(c) + b) * NQ + q) * 2]);
+  float acc = 0.f, L = 0.f;
+  for (int c = c0; c <= c1; ++c) {
+    if (!owns(c)) continue;
+    const size_t slot = static_cast<size_t>(c) + b;
+    const float w = fast_exp2(part_ml[(slot * NQ + q) * 2] - M);
+    L = fmaf(w, part_ml[(slot * NQ + q) * 2 + 1], L);
+    acc = fmaf(w, part_o[(slot * NQ + q) * 128 + d], acc);
+  }
+  *out = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+}
+
+}  // namespace b200

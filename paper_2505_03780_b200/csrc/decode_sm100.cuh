@@ -296,6 +296,18 @@ __global__ void __launch_bounds__(DecodeCfg<NSTAGE>::NTHREADS)
         asm volatile("st.shared.b16 [%0], %1;" ::"r"(addr), "h"(*reinterpret_cast<const uint16_t*>(&v))
                      : "memory");
       }
+      if (!valid) {
+        // tail slots of the last page hold arbitrary bytes: P = 0 there, but 0 * NaN would
+        // poison O, so zero this token's V row before PV reads it
+        const int vidx = 2 * i + 1, vslot = vidx % NSTAGE;
+        mbar_wait(&kv_full[vslot], (vidx / NSTAGE) & 1);
+        uint4* vr = reinterpret_cast<uint4*>(sKV + vslot * C::SLOT + t * 128);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          vr[c] = make_uint4(0, 0, 0, 0);
+          vr[C::HALF / 16 + c] = make_uint4(0, 0, 0, 0);
+        }
+      }
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&p_full[sb]);

@@ -25,7 +25,8 @@ PREFILL_DEFAULT = {"BLOCK_M": 256, "BLOCK_N": 128, "num_warps": 4, "num_stages":
                    "PRE_LOAD_V": False}
 PREFILL_FIXED_BASELINE = {"BLOCK_M": 128, "BLOCK_N": 128, "num_warps": 4, "num_stages": 2, "waves_per_eu": 1,
                           "PRE_LOAD_V": False}
-DECODE_DEFAULT = {"num_splits": 0, "num_stages": 4, "TILE_N": 128}
+DECODE_DEFAULT = {"num_splits": 0, "num_stages": 5, "TILE_N": 16}  # flat partition, 8 kv heads per tile
+DECODE_SPLIT_DEFAULT = {"num_splits": 0, "num_stages": 4, "TILE_N": 128}  # any geometry
 
 _GEOM = ("num_q_heads", "num_kv_heads", "head_dim", "block_size", "causal")
 
@@ -98,5 +99,18 @@ def default_prefill_config(**dims) -> dict:
     return dict(cfg)
 
 
+def flat_decode_ok(num_q_heads=32, num_kv_heads=8, block_size=16, batch_size=1, **_) -> bool:
+    """Shapes the TILE_N=16 flat-partition kernel is compiled for (else the per-head split kernel)."""
+    return (num_kv_heads == 8 and num_q_heads // num_kv_heads in (1, 2, 4, 8) and num_q_heads % 8 == 0
+            and block_size >= 16 and batch_size <= 1024)
+
+
 def default_decode_config(**dims) -> dict:
-    return dict(lookup("decode", dims) or DECODE_DEFAULT)
+    cfg = lookup("decode", dims)
+    if cfg is None:
+        cfg = DECODE_DEFAULT if flat_decode_ok(**dims) else DECODE_SPLIT_DEFAULT
+    if cfg.get("TILE_N") == 16 and not flat_decode_ok(**dims):
+        cfg = DECODE_SPLIT_DEFAULT
+    if cfg.get("TILE_N") == 16 and dims.get("num_q_heads", 32) // 8 == 8 and cfg.get("num_stages", 4) > 4:
+        cfg = dict(cfg, num_stages=4)  # 64 q heads: Q/P buffers leave room for 4 ring slots
+    return dict(cfg)
