@@ -360,9 +360,10 @@ def run_b200(args, world, rank, local):
         k_ms = cuda_time(gp.replay, 10, stream) / 20
         achieved = alg_bytes / (k_ms / 1e3) / 1e9
         peak = pk["hbm_gbs"]
-        tr = ncu_traffic("decode_split_kernel")
+        kname = "decode_flat_kernel" if int(plan.config["TILE_N"]) == 16 else "decode_split_kernel"
+        tr = ncu_traffic(kname)
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": tr, "kernel": "decode_split_kernel (K2)", "kernel_ms": k_ms,
+                    "traffic": tr, "kernel": f"{kname} (K2)", "kernel_ms": k_ms,
                     "algorithmic_bytes_per_launch": alg_bytes, "peak_kind": pk_kind}
     else:
         k_ms = ms / args.steps
