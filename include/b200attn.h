@@ -47,7 +47,7 @@ typedef struct {
   int32_t block_m;      /* BLOCK_M: query rows per CTA summed over its q heads: 128 (1 tile) | 256 (head pair) */
   int32_t block_n;      /* BLOCK_N: KV rows per pipeline step: 64 | 128                                         */
   int32_t num_warps;    /* softmax warps per 128-row Q tile: 4 (one thread per TMEM lane)                        */
-  int32_t num_stages;   /* depth of the K/V TMA ring (32-KB / 16-KB slots)                                       */
+  int32_t num_stages;   /* K/V ring = (num_stages + 1) x 32 KB of TMA slots (BLOCK_N rows of K or V each)         */
   int32_t waves_per_eu; /* AMD occupancy hint; only 1 is meaningful on sm_100a                                   */
   int32_t pre_load_v;   /* V_j is always issued right behind K_j on the shared ring; accepted for parity         */
 } b200attn_prefill_variant;
@@ -67,6 +67,8 @@ typedef struct {
   int32_t head_dim;           /* 128 */
   int32_t causal;             /* 1: key j attends iff j <= query position (q_len == k_len) */
   float softmax_scale;        /* <= 0 -> 1/sqrt(head_dim) */
+  void* workspace;            /* longest-first work list; b200attn_prefill_workspace_size bytes */
+  size_t workspace_bytes;
 } b200attn_prefill_params;
 
 /* One point of spaces/paged_decode.space.json. */
@@ -107,7 +109,8 @@ int b200attn_prefill_supported(const b200attn_prefill_params* p, const b200attn_
 int b200attn_decode_supported(const b200attn_decode_params* p, const b200attn_decode_variant* v,
                               char* reason, size_t reason_len);
 
-/* K1: causal (or full) varlen prefill. */
+/* K1: causal (or full) varlen prefill (schedule kernel + persistent attention kernel). */
+size_t b200attn_prefill_workspace_size(const b200attn_prefill_params* p);
 int b200attn_prefill(const b200attn_prefill_params* p, const b200attn_prefill_variant* v, void* stream);
 
 /* K2 (+K3): paged split-KV decode; the combine runs iff the resolved num_splits > 1. */
@@ -134,6 +137,7 @@ int b200attn_cache_append(const void* new_k, const void* new_v, void* k_cache, v
  *   mode 0: D[128x128]  = A[128x128] . B[128x128]^T   A, B K-major
  *   mode 1: D[128x128]  = A[128x128] . B[128x128]     B MN-major ([K][N] row-major)
  *   mode 2: D[128x16]   = A^T . B^T   with A [128(K)][128(M)] MN-major, B [16][128] K-major
+ *   mode 3: D[128x128]  = A . B^T     with A staged in TMEM (bf16x2 per column), B K-major (TS MMA)
  * A, B bf16 device pointers; D fp32 device pointer. */
 int b200attn_selftest_umma(int mode, const void* a, const void* b, float* d, void* stream);
 

@@ -33,7 +33,8 @@ class PrefillVariant(ctypes.Structure):
 class PrefillParams(ctypes.Structure):
     _fields_ = [("q", _P), ("k", _P), ("v", _P), ("o", _P), ("cu_seqlens", _P), ("lse", _P), ("num_seqs", _I),
                 ("total_tokens", _I), ("max_seqlen", _I), ("num_q_heads", _I), ("num_kv_heads", _I),
-                ("head_dim", _I), ("causal", _I), ("softmax_scale", ctypes.c_float)]
+                ("head_dim", _I), ("causal", _I), ("softmax_scale", ctypes.c_float), ("workspace", _P),
+                ("workspace_bytes", ctypes.c_size_t)]
 
 
 class DecodeVariant(ctypes.Structure):
@@ -63,7 +64,7 @@ STATUS_NAMES = {OK: "ok", UNSUPPORTED_CONFIG: "unsupported_config", SMEM_OVERFLO
 # every symbol include/b200attn.h declares (tests check the library exports all of them)
 EXPORTS = (
     "b200attn_abi_version", "b200attn_build_info", "b200attn_status_string", "b200attn_last_error",
-    "b200attn_prefill_supported", "b200attn_decode_supported", "b200attn_prefill",
+    "b200attn_prefill_supported", "b200attn_decode_supported", "b200attn_prefill_workspace_size", "b200attn_prefill",
     "b200attn_decode_workspace_size", "b200attn_decode_num_splits", "b200attn_decode", "b200attn_decode_partial",
     "b200attn_combine",
     "b200attn_cache_append", "b200attn_selftest_umma",
@@ -91,6 +92,8 @@ def load():
     lib.b200attn_prefill_supported.argtypes = [PP, PV, ctypes.c_char_p, ctypes.c_size_t]
     lib.b200attn_decode_supported.argtypes = [DP, DV, ctypes.c_char_p, ctypes.c_size_t]
     lib.b200attn_prefill.argtypes = [PP, PV, _P]
+    lib.b200attn_prefill_workspace_size.argtypes = [PP]
+    lib.b200attn_prefill_workspace_size.restype = ctypes.c_size_t
     lib.b200attn_decode.argtypes = [DP, DV, _P]
     lib.b200attn_decode_partial.argtypes = [DP, DV, _P]
     lib.b200attn_decode_workspace_size.argtypes = [DP, DV]

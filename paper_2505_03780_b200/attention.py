@@ -71,7 +71,7 @@ def prefill_supported(q_shape, kv_heads, num_seqs, max_seqlen, config: Mapping, 
     lib = _native.load()
     T, Hq, D = q_shape
     p = _native.PrefillParams(None, None, None, None, None, None, num_seqs, T, max_seqlen, Hq, kv_heads, D,
-                              int(causal), 0.0)
+                              int(causal), 0.0, None, 0)
     buf = _native.reason_buffer()
     rc = lib.b200attn_prefill_supported(p, prefill_variant(config), buf, len(buf))
     return rc, buf.value.decode()
@@ -101,6 +101,8 @@ def prefill_varlen(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, cu_seqlens
                                         max_seqlen=int(max_seqlen), num_q_heads=q.shape[1],
                                         num_kv_heads=k.shape[1], head_dim=q.shape[2], causal=causal)
     p = _prefill_params(q, k, v, out, cu_seqlens, max_seqlen, softmax_scale, causal, lse)
+    ws = _workspace(q.device, lib.b200attn_prefill_workspace_size(p), kind="prefill")
+    p.workspace, p.workspace_bytes = ws.data_ptr(), ws.numel()
     _native.check(lib.b200attn_prefill(p, prefill_variant(config), torch.cuda.current_stream(q.device).cuda_stream))
     return (out, lse) if return_lse else out
 
@@ -108,10 +110,10 @@ def prefill_varlen(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, cu_seqlens
 _workspaces: dict = {}
 
 
-def _workspace(device, nbytes: int) -> Optional[torch.Tensor]:
+def _workspace(device, nbytes: int, kind: str = "decode") -> Optional[torch.Tensor]:
     if nbytes == 0:
         return None
-    key = (device.type, device.index)
+    key = (device.type, device.index, kind)
     buf = _workspaces.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
@@ -274,6 +276,9 @@ class PrefillPlan:
             num_q_heads=q.shape[1], num_kv_heads=k.shape[1], head_dim=q.shape[2], causal=causal))
         self.var = prefill_variant(self.config)
         self.p = _prefill_params(q, k, v, self.out, cu_seqlens, max_seqlen, softmax_scale, causal, None)
+        self.ws = torch.empty(max(1, self.lib.b200attn_prefill_workspace_size(self.p)), dtype=torch.uint8,
+                              device=q.device)
+        self.p.workspace, self.p.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
         self.device = q.device
 
     def run(self, stream=None):

@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 
 #include "../../include/b200attn.h"
@@ -78,13 +79,23 @@ int make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint
   return B200ATTN_OK;
 }
 
+int num_sms();
+
 // ------------------------------------------------------------------ prefill variants
 using PrefillLauncher = int (*)(const b200attn_prefill_params*, cudaStream_t);
+constexpr int kPrefillEmu = 4;  // one element in 4 takes the FMA-pipe exp2
+
+size_t prefill_ws_ints(const b200attn_prefill_params* p, int* nkeys_out) {
+  const int nkeys = (p->max_seqlen + 127) / 128;
+  const size_t pairs = (size_t)p->total_tokens / 128 + (size_t)p->num_seqs + 1;
+  if (nkeys_out) *nkeys_out = nkeys;
+  return 2 + (size_t)nkeys + pairs;
+}
 
 template <int NQ, int BN, int NS>
 int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   using C = b200::PrefillCfg<NQ, BN, NS>;
-  auto kern = b200::prefill_fwd_kernel<NQ, BN, NS>;
+  auto kern = b200::prefill_fwd_kernel<NQ, BN, NS, kPrefillEmu>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -103,20 +114,30 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   if ((rc = make_map_3d(&mv, p->v, D, p->num_kv_heads, p->total_tokens, D * 2ull,
                         (uint64_t)p->num_kv_heads * D * 2, 1, BN)))
     return rc;
+  int nkeys = 0;
+  prefill_ws_ints(p, &nkeys);
+  int32_t* ws = reinterpret_cast<int32_t*>(p->workspace);
+  b200::prefill_schedule_kernel<<<1, 1024, 0, stream>>>(p->cu_seqlens, p->num_seqs, p->causal, nkeys, ws);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "prefill schedule launch");
   b200::PrefillKernelArgs a;
   a.cu_seqlens = p->cu_seqlens;
+  a.items = ws + 2 + nkeys;
+  a.sched = ws;
   a.o = reinterpret_cast<__nv_bfloat16*>(p->o);
   a.lse = p->lse;
   a.total_tokens = p->total_tokens;
   a.num_q_heads = p->num_q_heads;
   a.group = p->num_q_heads / p->num_kv_heads;
   a.causal = p->causal;
+  a.num_hg = p->num_q_heads / NQ;
   const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / sqrtf((float)p->head_dim);
   a.scale_log2 = scale * 1.4426950408889634f;
-  const int max_qblk = (p->max_seqlen + C::BM - 1) / C::BM;
-  dim3 grid(p->num_q_heads / NQ, max_qblk, p->num_seqs);
-  kern<<<grid, C::NTHREADS, C::SMEM_BYTES, stream>>>(mq, mk, mv, a);
-  cudaError_t e = cudaGetLastError();
+  // persistent: never more CTAs than work items (upper bound without a device read)
+  const long long items_ub = ((long long)p->total_tokens / 128 + p->num_seqs) * a.num_hg;
+  const int ctas = (int)std::min<long long>(num_sms(), std::max<long long>(1, items_ub));
+  kern<<<ctas, C::NTHREADS, C::SMEM_BYTES, stream>>>(mq, mk, mv, a);
+  e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
   return B200ATTN_OK;
 }
@@ -129,16 +150,11 @@ struct PrefillEntry {
 
 #define PF(NQ, BN, NS) {NQ, BN, NS, &launch_prefill<NQ, BN, NS>, b200::PrefillCfg<NQ, BN, NS>::SMEM_BYTES}
 const PrefillEntry kPrefill[] = {
-    PF(2, 128, 2), PF(2, 128, 3), PF(2, 64, 2), PF(2, 64, 3), PF(2, 64, 4),
-    PF(1, 128, 2), PF(1, 128, 3), PF(1, 128, 4), PF(1, 64, 2), PF(1, 64, 3), PF(1, 64, 4),
+    PF(2, 128, 1), PF(2, 128, 2), PF(2, 128, 3), PF(2, 128, 4), PF(2, 64, 1), PF(2, 64, 2), PF(2, 64, 3),
+    PF(2, 64, 4),  PF(1, 128, 1), PF(1, 128, 2), PF(1, 128, 3), PF(1, 128, 4), PF(1, 64, 1), PF(1, 64, 2),
+    PF(1, 64, 3),  PF(1, 64, 4),
 };
 #undef PF
-
-int prefill_smem_bytes(int nq, int bn, int ns) {
-  // same formula as PrefillCfg (kept here so unsupported stage counts can be diagnosed)
-  const int q = nq * 128 * 128 * 2, kv = ns * bn * 128 * 2, pb = nq * 128 * bn * 2;
-  return q + kv + pb + (1 + 2 * ns + 2 * nq + 1) * 8 + 16 + 1024;
-}
 
 int check_prefill(const b200attn_prefill_params* p, const b200attn_prefill_variant* v, const PrefillEntry** out) {
   if (!p || !v) return fail(B200ATTN_BAD_ARGS, "null params/variant");
@@ -158,18 +174,15 @@ int check_prefill(const b200attn_prefill_params* p, const b200attn_prefill_varia
                 "waves_per_eu=%d: AMD occupancy hint; one attention CTA owns an SM's TMEM on sm_100a",
                 v->waves_per_eu);
   const int nq = v->block_m / 128;
-  if (v->num_stages < 2)
-    return fail(B200ATTN_UNSUPPORTED_CONFIG, "num_stages=%d: the K/V ring needs >= 2 slots", v->num_stages);
-  const int smem = prefill_smem_bytes(nq, v->block_n, v->num_stages);
-  if (smem > kMaxSmem)
-    return fail(B200ATTN_SMEM_OVERFLOW, "shared memory %d B > %d B (BLOCK_M=%d BLOCK_N=%d num_stages=%d)", smem,
-                kMaxSmem, v->block_m, v->block_n, v->num_stages);
   const PrefillEntry* e = nullptr;
   for (const auto& x : kPrefill)
     if (x.nq == nq && x.bn == v->block_n && x.ns == v->num_stages) e = &x;
   if (!e)
     return fail(B200ATTN_UNSUPPORTED_CONFIG, "no compiled variant for BLOCK_M=%d BLOCK_N=%d num_stages=%d",
                 v->block_m, v->block_n, v->num_stages);
+  if (e->smem > kMaxSmem)
+    return fail(B200ATTN_SMEM_OVERFLOW, "shared memory %d B > %d B (BLOCK_M=%d BLOCK_N=%d num_stages=%d)",
+                e->smem, kMaxSmem, v->block_m, v->block_n, v->num_stages);
   if (p->head_dim != 128) return fail(B200ATTN_UNSUPPORTED_CONFIG, "head_dim=%d (compiled for 128)", p->head_dim);
   if (p->num_kv_heads <= 0 || p->num_q_heads <= 0 || p->num_q_heads % p->num_kv_heads)
     return fail(B200ATTN_BAD_ARGS, "num_q_heads=%d not a multiple of num_kv_heads=%d", p->num_q_heads,
@@ -472,6 +485,11 @@ int b200attn_prefill_supported(const b200attn_prefill_params* p, const b200attn_
   return rc;
 }
 
+size_t b200attn_prefill_workspace_size(const b200attn_prefill_params* p) {
+  if (!p) return 0;
+  return prefill_ws_ints(p, nullptr) * sizeof(int32_t);
+}
+
 int b200attn_prefill(const b200attn_prefill_params* p, const b200attn_prefill_variant* v, void* stream) {
   const PrefillEntry* e;
   g_err[0] = 0;
@@ -479,6 +497,9 @@ int b200attn_prefill(const b200attn_prefill_params* p, const b200attn_prefill_va
   if (rc) return rc;
   if (!p->q || !p->k || !p->v || !p->o || !p->cu_seqlens) return fail(B200ATTN_BAD_ARGS, "null tensor pointer");
   if (p->total_tokens == 0 || p->max_seqlen == 0) return B200ATTN_OK;
+  const size_t need = prefill_ws_ints(p, nullptr) * sizeof(int32_t);
+  if (!p->workspace || p->workspace_bytes < need)
+    return fail(B200ATTN_BAD_ARGS, "prefill workspace %zu B < %zu B", p->workspace_bytes, need);
   return e->fn(p, reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -574,7 +595,7 @@ int b200attn_cache_append(const void* new_k, const void* new_v, void* k_cache, v
 
 int b200attn_selftest_umma(int mode, const void* a, const void* b, float* d, void* stream) {
   g_err[0] = 0;
-  if (mode < 0 || mode > 2 || !a || !b || !d) return fail(B200ATTN_BAD_ARGS, "selftest args");
+  if (mode < 0 || mode > 3 || !a || !b || !d) return fail(B200ATTN_BAD_ARGS, "selftest args");
   cudaError_t ea = cudaFuncSetAttribute(b200::umma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         b200::kSelftestSmem);
   if (ea != cudaSuccess) return cuda_fail(ea, "cudaFuncSetAttribute(selftest)");

@@ -36,14 +36,39 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(const __nv_bfloat16*
     mbar_init(&bar, 1);
     fence_barrier_init();
   }
-  if (tid < 32) tmem_alloc(&tslot, 128);
+  if (tid < 32) tmem_alloc(&tslot, 256);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tslot;
   const int N = (mode == 2) ? 16 : 128;
-  if (tid == 0) {
+  if (mode == 3) {
+    // A -> TMEM columns [128, 192): lane r = row r, column c holds (A[r][2c] lo, A[r][2c+1] hi)
+    const uint32_t arow = tmem + 128 + (static_cast<uint32_t>((tid >> 5) << 5) << 16);
+    for (int c = 0; c < 4; ++c) {
+      uint32_t r[16];
+      for (int j = 0; j < 16; ++j) {
+        const __nv_bfloat16 lo = A[tid * 128 + c * 32 + 2 * j], hi = A[tid * 128 + c * 32 + 2 * j + 1];
+        r[j] = static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(&lo)) |
+               (static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(&hi)) << 16);
+      }
+      tmem_st16(arow + c * 16, r);
+    }
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  if (tid == 0 && mode == 3) {
+    const uint32_t b0 = smem_u32(sB);
+    const uint32_t idesc = idesc_bf16_f32(128, 128, false, false);
+    for (int kk = 0; kk < 8; ++kk) {
+      const uint64_t db = sdesc_sw128(b0 + (kk >> 2) * 128 * 128 + (kk & 3) * 32, 16, 1024);
+      umma_ts(tmem, tmem + 128 + kk * 8, db, idesc, kk > 0);
+    }
+    umma_commit(&bar);
+  } else if (tid == 0) {
     const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
     const uint32_t idesc = idesc_bf16_f32(128, N, mode == 2, mode == 1);
     for (int kk = 0; kk < 8; ++kk) {
@@ -74,7 +99,7 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(const __nv_bfloat16*
   __syncthreads();
   if (tid < 32) {
     tc_fence_after();
-    tmem_dealloc(tmem, 128);
+    tmem_dealloc(tmem, 256);
   }
 }
 

@@ -47,7 +47,7 @@ def cfg(**kw):
 def test_prefill_supported_accepts_compiled_variants():
     for bm in (128, 256):
         for bn in (64, 128):
-            for ns in (2, 3):
+            for ns in (1, 2, 3, 4):
                 rc, why = A.prefill_supported(config=cfg(BLOCK_M=bm, BLOCK_N=bn, num_stages=ns), **C1)
                 assert rc == _native.OK, why
 
@@ -57,8 +57,7 @@ def test_prefill_supported_accepts_compiled_variants():
     (dict(BLOCK_N=32, BLOCK_M=128), _native.UNSUPPORTED_CONFIG),
     (dict(num_warps=8), _native.UNSUPPORTED_CONFIG),
     (dict(waves_per_eu=2), _native.UNSUPPORTED_CONFIG),
-    (dict(num_stages=1), _native.UNSUPPORTED_CONFIG),
-    (dict(num_stages=4), _native.SMEM_OVERFLOW),
+    (dict(num_stages=5), _native.UNSUPPORTED_CONFIG),
 ])
 def test_prefill_rejections(kw, code):
     rc, why = A.prefill_supported(config=cfg(**kw), **C1)
@@ -82,8 +81,8 @@ def test_flash_attention_space_variant_map():
         ok += rc == _native.OK
         if rc != _native.OK:
             assert why
-    # 4 (128/64) + 4 (128/128) + 4 (256/64) + 3 (256/128: stages 2,3; 4 overflows smem); PRE_LOAD_V only with stages<=2
-    assert ok == 15
+    # BLOCK_M {128,256} x BLOCK_N {64,128} x num_stages 1..4 (x PRE_LOAD_V, which needs stages <= 2)
+    assert ok == 24
 
 
 def test_decode_supported_and_splits():
