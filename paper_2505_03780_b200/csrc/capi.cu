@@ -83,7 +83,7 @@ int num_sms();
 
 // ------------------------------------------------------------------ prefill variants
 using PrefillLauncher = int (*)(const b200attn_prefill_params*, cudaStream_t);
-constexpr int kPrefillEmu = 4;  // one element in 4 takes the FMA-pipe exp2
+constexpr int kPrefillEmu = 0;  // measured: MUFU is not the limiter (EMU 0: 966, 8: 934, 4: 906, 2: 840 TFLOP/s on C3)
 
 size_t prefill_ws_ints(const b200attn_prefill_params* p, int* nkeys_out) {
   const int nkeys = (p->max_seqlen + 127) / 128;

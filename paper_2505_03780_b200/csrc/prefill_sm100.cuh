@@ -93,6 +93,65 @@ __device__ __forceinline__ void prefill_decode_item(int w, const PrefillKernelAr
   qblk = it & 0xFFFF;
 }
 
+// Pass 2 over one S row: P = exp2(S*sl2 - m) -> bf16 pairs written back over the S columns;
+// returns the row sum.  MASKED is a compile-time split so the common (interior) tile carries no
+// per-element compare/select at all — predicated-off instructions still cost issue slots.
+template <int BN, bool MASKED>
+__device__ __forceinline__ float softmax_pass2(uint32_t s_addr, float sl2, float nmu, int kv0, int lim) {
+  float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+  for (int c = 0; c < BN / 64; ++c) {
+    uint32_t ra[32], rb[32];
+    tmem_ld32x2(s_addr + c * 64, s_addr + c * 64 + 32, ra, rb);
+    uint32_t pa[16], pb[16];
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const uint32_t* r = half ? rb : ra;
+      uint32_t* pk = half ? pb : pa;
+      const int col0 = kv0 + c * 64 + half * 32;
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        float x0, x1;
+        ffma2(x0, x1, __uint_as_float(r[i]), __uint_as_float(r[i + 1]), sl2, nmu);
+        float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
+        if constexpr (MASKED) {
+          if (col0 + i > lim) e0 = 0.f;
+          if (col0 + i + 1 > lim) e1 = 0.f;
+        }
+        fadd2(ls0, ls1, e0, e1);
+        pk[i >> 1] = pack_bf16x2(e0, e1);
+      }
+    }
+    tmem_st16(s_addr + c * 32, pa);  // P overwrites S columns this thread has already read
+    tmem_st16(s_addr + c * 32 + 16, pb);
+  }
+  return ls0 + ls1;
+}
+
+template <int BN, bool MASKED>
+__device__ __forceinline__ float softmax_rowmax(uint32_t s_addr, int kv0, int lim) {
+  float mt = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < BN / 64; ++c) {
+    uint32_t ra[32], rb[32];
+    tmem_ld32x2(s_addr + c * 64, s_addr + c * 64 + 32, ra, rb);
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      if constexpr (MASKED) {
+        const int ca = kv0 + c * 64 + i, cb = ca + 32;
+        mt = fmaxf(mt, fmaxf(ca > lim ? -INFINITY : __uint_as_float(ra[i]),
+                             ca + 1 > lim ? -INFINITY : __uint_as_float(ra[i + 1])));
+        mt = fmaxf(mt, fmaxf(cb > lim ? -INFINITY : __uint_as_float(rb[i]),
+                             cb + 1 > lim ? -INFINITY : __uint_as_float(rb[i + 1])));
+      } else {
+        mt = fmaxf(mt, fmaxf(__uint_as_float(ra[i]), __uint_as_float(ra[i + 1])));
+        mt = fmaxf(mt, fmaxf(__uint_as_float(rb[i]), __uint_as_float(rb[i + 1])));
+      }
+    }
+  }
+  return mt;
+}
+
 template <int NQ, int BN, int NSTAGE_CFG, int EMU>
 __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
     prefill_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
@@ -301,30 +360,8 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
         // masking is only needed on the diagonal / last tile: decide per warp, keep the common
         // path free of per-element compares and selects
         const bool warp_edge = __any_sync(0xffffffffu, edge);
-        float mt = -INFINITY;
-        if (!warp_edge) {
-#pragma unroll
-          for (int c = 0; c < BN / 64; ++c) {
-            uint32_t ra[32], rb[32];
-            tmem_ld32x2(s_addr + c * 64, s_addr + c * 64 + 32, ra, rb);
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              mt = fmaxf(mt, fmaxf(__uint_as_float(ra[i]), __uint_as_float(ra[i + 1])));
-              mt = fmaxf(mt, fmaxf(__uint_as_float(rb[i]), __uint_as_float(rb[i + 1])));
-            }
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < BN / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(s_addr + c * 32, r);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float v = (kv0 + c * 32 + i > lim) ? -INFINITY : __uint_as_float(r[i]);
-              mt = fmaxf(mt, v);
-            }
-          }
-        }
+        const float mt = warp_edge ? softmax_rowmax<BN, true>(s_addr, kv0, lim)
+                                   : softmax_rowmax<BN, false>(s_addr, kv0, lim);
         const float m_new = fmaxf(m_run, mt * sl2);
         const bool need = (m_new > m_run + 8.0f);
         float alpha = 1.f;
@@ -344,39 +381,8 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
           }
         }
         const float nmu = (m_run == -INFINITY) ? 0.f : -m_run;
-        float ls0 = 0.f, ls1 = 0.f;
-#pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(s_addr + c * 32, r);
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            float x0, x1;
-            ffma2(x0, x1, __uint_as_float(r[i]), __uint_as_float(r[i + 1]), sl2, nmu);
-            float e0, e1;
-            if constexpr (EMU > 0) {
-              if ((i >> 1) % EMU == EMU - 1) {
-                e0 = exp2_poly(x0);
-                e1 = exp2_poly(x1);
-              } else {
-                e0 = fast_exp2(x0);
-                e1 = fast_exp2(x1);
-              }
-            } else {
-              e0 = fast_exp2(x0);
-              e1 = fast_exp2(x1);
-            }
-            if (warp_edge) {
-              if (kv0 + c * 32 + i > lim) e0 = 0.f;
-              if (kv0 + c * 32 + i + 1 > lim) e1 = 0.f;
-            }
-            fadd2(ls0, ls1, e0, e1);
-            pk[i >> 1] = pack_bf16x2(e0, e1);
-          }
-          tmem_st16(s_addr + c * 16, pk);  // P overwrites S columns this thread has already read
-        }
-        const float lsum = ls0 + ls1;
+        const float lsum = warp_edge ? softmax_pass2<BN, true>(s_addr, sl2, nmu, kv0, lim)
+                                     : softmax_pass2<BN, false>(s_addr, sl2, nmu, kv0, lim);
         l_run += lsum;
         tmem_wait_st();
         tc_fence_before();
