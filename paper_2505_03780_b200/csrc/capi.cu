@@ -83,7 +83,7 @@ int num_sms();
 
 // ------------------------------------------------------------------ prefill variants
 using PrefillLauncher = int (*)(const b200attn_prefill_params*, cudaStream_t);
-constexpr int kPrefillEmu = 0;  // measured: MUFU is not the limiter (EMU 0: 966, 8: 934, 4: 906, 2: 840 TFLOP/s on C3)
+constexpr int kPrefillEmu = 3;  // 1 pair in 3 on the FMA pipe (C3: EMU 0: 987, 3: 1008, 4: 1003, 6: 1004 TFLOP/s)
 
 size_t prefill_ws_ints(const b200attn_prefill_params* p, int* nkeys_out) {
   const int nkeys = (p->max_seqlen + 127) / 128;
@@ -591,6 +591,37 @@ int b200attn_cache_append(const void* new_k, const void* new_v, void* k_cache, v
       (int64_t)num_blocks * block_size);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? B200ATTN_OK : cuda_fail(e, "cache_append launch");
+}
+
+#ifdef B200_TRACE
+int b200attn_debug_trace(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, b200::g_trace, sizeof(unsigned long long) * (size_t)n);
+}
+#endif
+
+int b200attn_debug_umma_rate(int mode, int iters, int ctas, long long* out_dev, void* stream) {
+  const int smem = 32768 + 65536 + 16 + 1024;
+  void (*k)(int, long long*) = nullptr;
+  switch (mode) {
+    case 0: k = b200::umma_rate_kernel<128, false, false>; break;
+    case 1: k = b200::umma_rate_kernel<128, true, true>; break;
+    case 2: k = b200::umma_rate_kernel<128, false, true>; break;
+    case 3: k = b200::umma_rate_kernel<256, false, false>; break;
+    case 4: k = b200::umma_rate_kernel<128, true, false>; break;
+    case 5: k = b200::umma_rate_kernel<64, false, false>; break;
+    case 6: k = b200::umma_rate_kernel<256, false, true>; break;
+    case 7: k = b200::umma_rate_kernel<64, true, true>; break;
+    case 8: k = b200::umma_rate_kernel<128, false, false, 4>; break;
+    case 9: k = b200::umma_rate_kernel<128, true, true, 4>; break;
+    case 10: k = b200::umma_rate_kernel<128, false, false, 8>; break;
+    default: return fail(B200ATTN_BAD_ARGS, "mode");
+  }
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "attr");
+  const int threads = mode == 10 ? 384 : (mode >= 8 ? 256 : 128);
+  k<<<ctas, threads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(iters, out_dev);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? B200ATTN_OK : cuda_fail(e, "umma_rate launch");
 }
 
 int b200attn_selftest_umma(int mode, const void* a, const void* b, float* d, void* stream) {

@@ -198,24 +198,22 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
       t = seg_end;
     }
   } else if (warp == C::MMA_WARP) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (whole warp, one elected lane issues)
+    {
       constexpr uint32_t IDESC_QK = idesc_bf16_f32(C::ROWS, NP, false, false);
       constexpr uint32_t IDESC_PV = idesc_bf16_f32(D, NP, true, false);
-      const uint32_t kv_base = smem_u32(sKV), q_base = smem_u32(sQ), p_base = smem_u32(sP);
+      const uint64_t k_desc = sdesc_sw128(smem_u32(sKV), 16, 1024);
+      const uint64_t v_desc = sdesc_sw128(smem_u32(sKV), C::HALF, 1024);
+      const uint64_t q_desc = sdesc_sw128(smem_u32(sQ), 16, 1024);
+      const uint64_t p_desc = sdesc_sw128(smem_u32(sP), 16, 1024);
       auto qk = [&](int i, int qb) {
         const int idx = 2 * i, slot = idx % NSTAGE;
         mbar_wait(&kv_full[slot], (idx / NSTAGE) & 1);
         tc_fence_after();
-        const uint32_t kb = kv_base + slot * C::SLOT, qa = q_base + qb * C::QB;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t da = sdesc_sw128(kb + (kk >> 2) * C::HALF + (kk & 3) * 32, 16, 1024);
-          const uint64_t db = sdesc_sw128(qa + (kk >> 2) * C::QHALF + (kk & 3) * 32, 16, 1024);
-          umma_ss(tmem + C::S_COL(i), da, db, IDESC_QK, kk > 0);
-        }
-        umma_commit(&s_full[i & 1]);
-        umma_commit(&kv_empty[slot]);
+        const uint64_t kb = k_desc + ((slot * C::SLOT) >> 4), qa = q_desc + ((qb * C::QB) >> 4);
+        umma_ss_k128<2, C::HALF / 16, 2, C::QHALF / 16>(tmem + C::S_COL(i), kb, qa, IDESC_QK, 0u);
+        umma_commit_w(&s_full[i & 1]);
+        umma_commit_w(&kv_empty[slot]);
       };
       auto pv = [&](int i) {
         const int idx = 2 * i + 1, slot = idx % NSTAGE;
@@ -223,15 +221,10 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
         mbar_wait(&p_full[i & 1], (i >> 1) & 1);
         if (i >= 2) mbar_wait(&o_empty[i & 1], ((i >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t vb = kv_base + slot * C::SLOT, pb = p_base + (i & 1) * C::PB;
-#pragma unroll
-        for (int kk = 0; kk < C::ROWS / 16; ++kk) {
-          const uint64_t da = sdesc_sw128(vb + kk * 16 * 128, C::HALF, 1024);
-          const uint64_t db = sdesc_sw128(pb + (kk >> 2) * C::PHALF + (kk & 3) * 32, 16, 1024);
-          umma_ss(tmem + C::O_COL(i), da, db, IDESC_PV, kk > 0);
-        }
-        umma_commit(&o_full[i & 1]);
-        umma_commit(&kv_empty[slot]);
+        const uint64_t vb = v_desc + ((slot * C::SLOT) >> 4), pb = p_desc + (((i & 1) * C::PB) >> 4);
+        umma_ss_k128<128, 512, 2, C::PHALF / 16>(tmem + C::O_COL(i), vb, pb, IDESC_PV, 0u);
+        umma_commit_w(&o_full[i & 1]);
+        umma_commit_w(&kv_empty[slot]);
       };
       int i = 0, k = 0, b = b_first;
       for (int t = T0; t < T1; ++k) {
@@ -240,7 +233,7 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
         mbar_wait(&q_full[k & 1], (k >> 1) & 1);
         for (; t < seg_end; ++t, ++i) {
           qk(i, k & 1);
-          if (t == seg_end - 1) umma_commit(&q_empty[k & 1]);
+          if (t == seg_end - 1) umma_commit_w(&q_empty[k & 1]);
           if (i >= 1) pv(i - 1);
         }
       }

@@ -84,6 +84,27 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// Pair version on FFMA2/FADD2: ~5 issue slots per element instead of one MUFU.EX2 (8 MUFU-pipe
+// cycles per warp instruction), so a fraction of the exponentials can move off the MUFU pipe.
+__device__ __forceinline__ void exp2_poly2(float x0, float x1, float& y0, float& y1) {
+  x0 = fmaxf(x0, -126.0f);
+  x1 = fmaxf(x1, -126.0f);
+  const float shifter = 12582912.0f;
+  float t0, t1, n0, n1;
+  ffma2(t0, t1, x0, x1, 1.0f, shifter);
+  ffma2(n0, n1, t0, t1, 1.0f, -shifter);
+  float f0, f1;
+  ffma2(f0, f1, n0, n1, -1.0f, 0.0f);
+  fadd2(f0, f1, x0, x1);  // f = x - n
+  float p0 = 0.05517027899622917f, p1 = 0.05517027899622917f;
+  float q0, q1;
+  ffma2_v(q0, q1, p0, p1, f0, f1, 0.2426076978445053f);
+  ffma2_v(p0, p1, q0, q1, f0, f1, 0.693260908126831f);
+  ffma2_v(q0, q1, p0, p1, f0, f1, 0.9999282956123352f);
+  y0 = __int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23));
+  y1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
+}
+
 __device__ __forceinline__ void prefill_decode_item(int w, const PrefillKernelArgs& a, int& seq, int& qblk,
                                                     int& hg) {
   const int pair = w / a.num_hg;
@@ -96,7 +117,7 @@ __device__ __forceinline__ void prefill_decode_item(int w, const PrefillKernelAr
 // Pass 2 over one S row: P = exp2(S*sl2 - m) -> bf16 pairs written back over the S columns;
 // returns the row sum.  MASKED is a compile-time split so the common (interior) tile carries no
 // per-element compare/select at all — predicated-off instructions still cost issue slots.
-template <int BN, bool MASKED>
+template <int BN, bool MASKED, int EMU>
 __device__ __forceinline__ float softmax_pass2(uint32_t s_addr, float sl2, float nmu, int kv0, int lim) {
   float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
@@ -113,7 +134,18 @@ __device__ __forceinline__ float softmax_pass2(uint32_t s_addr, float sl2, float
       for (int i = 0; i < 32; i += 2) {
         float x0, x1;
         ffma2(x0, x1, __uint_as_float(r[i]), __uint_as_float(r[i + 1]), sl2, nmu);
-        float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
+        float e0, e1;
+        if constexpr (!MASKED && EMU > 0) {
+          if ((i >> 1) % EMU == EMU - 1) {
+            exp2_poly2(x0, x1, e0, e1);
+          } else {
+            e0 = fast_exp2(x0);
+            e1 = fast_exp2(x1);
+          }
+        } else {
+          e0 = fast_exp2(x0);
+          e1 = fast_exp2(x1);
+        }
         if constexpr (MASKED) {
           if (col0 + i > lim) e0 = 0.f;
           if (col0 + i + 1 > lim) e1 = 0.f;
@@ -151,6 +183,19 @@ __device__ __forceinline__ float softmax_rowmax(uint32_t s_addr, int kv0, int li
   }
   return mt;
 }
+
+#ifdef B200_TRACE
+// debug-only event trace of CTA 0: [event][slot] clock64 stamps
+__device__ unsigned long long g_trace[8][512];
+#define TRACE(ev, slot)                                                        \
+  do {                                                                        \
+    if (blockIdx.x == 0 && (slot) < 512) g_trace[ev][slot] = clock64();        \
+  } while (0)
+#else
+#define TRACE(ev, slot) \
+  do {                  \
+  } while (0)
+#endif
 
 template <int NQ, int BN, int NSTAGE_CFG, int EMU>
 __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
@@ -251,34 +296,38 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
       }
     }
   } else if (warp == C::MMA_WARP) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (whole warp, one elected lane issues)
+    {
       constexpr uint32_t IDESC_QK = idesc_bf16_f32(BM, BN, false, false);
       constexpr uint32_t IDESC_PV = idesc_bf16_f32(BM, D, false, true);
-      const uint32_t q_base = smem_u32(sQ), kv_base = smem_u32(sKV);
+      // Descriptors are built once; per-MMA addressing is a 16-B-unit add on the start-address
+      // field (smem < 256 KB, so the 14-bit field never carries).  Rebuilding 64-bit descriptors
+      // per MMA costs the single issuing thread ~120 cycles and starves the tensor pipe.
+      const uint64_t q_desc = sdesc_sw128(smem_u32(sQ), 16, 1024);
+      const uint64_t k_desc = sdesc_sw128(smem_u32(sKV), 16, 1024);
+      const uint64_t v_desc = sdesc_sw128(smem_u32(sKV), C::HALF_KV, 1024);
       auto issue_qk = [&](int t, int slot) {
-        const uint32_t qa = q_base + t * C::Q_BYTES, kb = kv_base + slot * C::KV_BYTES;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk & 3) * 32;
-          const uint64_t da = sdesc_sw128(qa + (kk >> 2) * C::HALF_Q + off, 16, 1024);
-          const uint64_t db = sdesc_sw128(kb + (kk >> 2) * C::HALF_KV + off, 16, 1024);
-          umma_ss(tmem + C::S_COL(t), da, db, IDESC_QK, kk > 0);
-        }
+        const uint64_t qa = q_desc + ((t * C::Q_BYTES) >> 4);
+        const uint64_t kb = k_desc + ((slot * C::KV_BYTES) >> 4);
+        umma_ss_k128<2, C::HALF_Q / 16, 2, C::HALF_KV / 16>(tmem + C::S_COL(t), qa, kb, IDESC_QK, 0u);
       };
       auto issue_pv = [&](int t, int slot, bool acc) {
-        const uint32_t vb = kv_base + slot * C::KV_BYTES;
+        const uint64_t vb = v_desc + ((slot * C::KV_BYTES) >> 4);
+        if constexpr (BN == 128) {
+          umma_ts_k128<128, 512>(tmem + C::O_COL(t), tmem + C::S_COL(t), vb, IDESC_PV, acc ? 1u : 0u);
+        } else {
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t db = sdesc_sw128(vb + kk * 16 * 128, C::HALF_KV, 1024);
-          umma_ts(tmem + C::O_COL(t), tmem + C::S_COL(t) + kk * 8, db, IDESC_PV, (acc || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BN / 16; ++kk)
+            umma_ts_w(tmem + C::O_COL(t), tmem + C::S_COL(t) + kk * 8, vb + ((kk * 16 * 128) >> 4), IDESC_PV,
+                      (acc || kk > 0) ? 1u : 0u);
         }
       };
       int ri = 0, gt = 0;
       for (int k = 0;; ++k) {
         mbar_wait(&item_full[k & 1], (k >> 1) & 1);
         const int w = item_box[k & 1];
-        mbar_arrive(&item_empty[k & 1]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&item_empty[k & 1]);  // the MMA warp counts as one consumer
         if (w < 0) break;
         int seq, qblk, hg;
         prefill_decode_item(w, args, seq, qblk, hg);
@@ -291,40 +340,43 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
           tc_fence_after();
           for (int t = 0; t < NQ; ++t) {
             issue_qk(t, slot);
-            umma_commit(&s_full[t]);
+            umma_commit_w(&s_full[t]);
           }
-          umma_commit(&kv_empty[slot]);
-          if (n_kv == 1) umma_commit(q_empty);
+          umma_commit_w(&kv_empty[slot]);
+          if (n_kv == 1) umma_commit_w(q_empty);
           ++ri;
         }
         for (int j = 0; j < n_kv; ++j) {
           const int vslot = ri % NS;
           mbar_wait(&kv_full[vslot], (ri / NS) & 1);
+          TRACE(6, gt + j);
           ++ri;
           const bool more = (j + 1) < n_kv;
           const int kslot = ri % NS;
           for (int t = 0; t < NQ; ++t) {
             mbar_wait(&p_full[t], (gt + j) & 1);
+            TRACE(4 + t, gt + j);
             if (j == 0 && k > 0) mbar_wait(&o_free[t], (k - 1) & 1);
             tc_fence_after();
             issue_pv(t, vslot, j > 0);
-            if (t == NQ - 1) umma_commit(&kv_empty[vslot]);
+            if (t == NQ - 1) umma_commit_w(&kv_empty[vslot]);
             if (more) {
               if (t == 0) {
                 mbar_wait(&kv_full[kslot], (ri / NS) & 1);
                 tc_fence_after();
               }
               issue_qk(t, kslot);
-              umma_commit(&s_full[t]);
+              if (t == 0) TRACE(7, gt + j);
+              umma_commit_w(&s_full[t]);
               if (t == NQ - 1) {
-                umma_commit(&kv_empty[kslot]);
-                if (j + 2 == n_kv) umma_commit(q_empty);
+                umma_commit_w(&kv_empty[kslot]);
+                if (j + 2 == n_kv) umma_commit_w(q_empty);
               }
             }
           }
           if (more) ++ri;
         }
-        umma_commit(o_full);
+        umma_commit_w(o_full);
         gt += n_kv;
       }
     }
@@ -355,13 +407,20 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
       for (int j = 0; j < n_kv; ++j) {
         mbar_wait(&s_full[t], (gt + j) & 1);
         tc_fence_after();
+        if (row == 0) TRACE(t, gt + j);
         const int kv0 = j * BN;
         const bool edge = (kv0 + BN > kv_end) || (args.causal && kv0 + BN - 1 > q_pos);
         // masking is only needed on the diagonal / last tile: decide per warp, keep the common
         // path free of per-element compares and selects
         const bool warp_edge = __any_sync(0xffffffffu, edge);
+#ifdef B200_EXPT_NO_PASS1
+        const float mt = (j == 0 || warp_edge) ? (warp_edge ? softmax_rowmax<BN, true>(s_addr, kv0, lim)
+                                                            : softmax_rowmax<BN, false>(s_addr, kv0, lim))
+                                               : m_run / sl2;
+#else
         const float mt = warp_edge ? softmax_rowmax<BN, true>(s_addr, kv0, lim)
                                    : softmax_rowmax<BN, false>(s_addr, kv0, lim);
+#endif
         const float m_new = fmaxf(m_run, mt * sl2);
         const bool need = (m_new > m_run + 8.0f);
         float alpha = 1.f;
@@ -381,11 +440,12 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
           }
         }
         const float nmu = (m_run == -INFINITY) ? 0.f : -m_run;
-        const float lsum = warp_edge ? softmax_pass2<BN, true>(s_addr, sl2, nmu, kv0, lim)
-                                     : softmax_pass2<BN, false>(s_addr, sl2, nmu, kv0, lim);
+        const float lsum = warp_edge ? softmax_pass2<BN, true, EMU>(s_addr, sl2, nmu, kv0, lim)
+                                     : softmax_pass2<BN, false, EMU>(s_addr, sl2, nmu, kv0, lim);
         l_run += lsum;
         tmem_wait_st();
         tc_fence_before();
+        if (row == 0) TRACE(2 + t, gt + j);
         mbar_arrive(&p_full[t]);
       }
 

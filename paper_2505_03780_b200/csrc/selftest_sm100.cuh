@@ -121,3 +121,77 @@ __global__ void cache_append_kernel(const uint4* __restrict__ nk, const uint4* _
 }
 
 }  // namespace b200
+
+namespace b200 {
+// MMA throughput probe (timing only; operands are whatever is in smem/TMEM).
+// A_TMEM: A operand from TMEM (TS) else smem K-major; B_MN: B operand MN-major else K-major.
+// Descriptors are precomputed so the single issuing thread only issues tcgen05.mma.
+template <int N, bool A_TMEM, bool B_MN, int LOAD_WARPS = 0>
+__global__ void __launch_bounds__(128 + 32 * LOAD_WARPS) umma_rate_kernel(int iters, long long* out) {
+  extern __shared__ uint8_t st_raw[];
+  uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(st_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sA + 32768;
+  uint64_t& bar = *reinterpret_cast<uint64_t*>(sB + 65536);
+  uint32_t& tslot = *reinterpret_cast<uint32_t*>(sB + 65536 + 8);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(&tslot, 512);
+  if (threadIdx.x == 0) *(&tslot + 1) = 0;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (threadIdx.x == 0) {
+    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+    constexpr uint32_t idesc = idesc_bf16_f32(128, N, false, B_MN);
+    uint64_t da[8], db[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      da[kk] = sdesc_sw128(a0 + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+      db[kk] = B_MN ? sdesc_sw128(b0 + kk * 2048, N == 256 ? 16384 : 16384, 1024)
+                    : sdesc_sw128(b0 + (kk >> 2) * N * 128 + (kk & 3) * 32, 16, 1024);
+    }
+    constexpr uint32_t DSTRIDE = N <= 128 ? 256 : 256;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const uint32_t d = tmem + (it & 1) * (N <= 128 ? 128 : 256);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        if constexpr (A_TMEM) umma_ts(d, tmem + 384 + kk * 8, db[kk], idesc, kk > 0);
+        else umma_ss(d, da[kk], db[kk], idesc, kk > 0);
+      }
+    }
+    umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    out[blockIdx.x] = (clock64() - t0) / iters;
+    (void)DSTRIDE;
+    *reinterpret_cast<volatile int*>(&tslot + 1) = 1;  // stop flag for the load warps
+  }
+  if constexpr (LOAD_WARPS > 0) {
+    // contention: warps 4.. stream tcgen05.ld + tcgen05.st over TMEM columns [256+..) like a
+    // softmax pass (read 64 cols, write 16 packed cols back)
+    if (threadIdx.x >= 128) {
+      const int w = (threadIdx.x >> 5) & 3;
+      const uint32_t base = tmem + (static_cast<uint32_t>(w << 5) << 16) + 448;
+      float acc = 0.f;
+      while (*reinterpret_cast<volatile int*>(&tslot + 1) == 0) {
+        uint32_t ra[32], rb[32];
+        tmem_ld32x2(base, base + 32, ra, rb);
+        uint32_t pk[16];
+        for (int i = 0; i < 16; ++i) pk[i] = ra[2 * i] ^ rb[2 * i + 1];
+        tmem_st16(base, pk);
+        acc += __uint_as_float(ra[0]);
+      }
+      if (acc == 12345.f) out[0] = 0;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+}  // namespace b200

@@ -149,6 +149,99 @@ __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-convergent variants: the whole warp executes them (operands warp-uniform, so they stay
+// in uniform registers) and one elected lane issues — no divergent wrapper per MMA.
+__device__ __forceinline__ void umma_ss_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+// Eight K=16 steps of one MMA (K = 128) in one asm block: operand k of step kk is
+// base + (kk & 3) * S + (kk >> 2) * H (16-byte descriptor units). Issued by one elected lane of a
+// convergent warp; keeps the issuing warp's instruction count (and SMSP pressure) minimal.
+template <int AS, int AH, int BS, int BH>
+__device__ __forceinline__ void umma_ss_k128(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred e, p;\n\t.reg .b64 ta, tb;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "setp.eq.u32 p, 0, 0;\n\t"
+      "add.s64 ta, %1, %5;\n\tadd.s64 tb, %2, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %7;\n\tadd.s64 tb, %2, %8;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %9;\n\tadd.s64 tb, %2, %10;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %11;\n\tadd.s64 tb, %2, %12;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %13;\n\tadd.s64 tb, %2, %14;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %15;\n\tadd.s64 tb, %2, %16;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %17;\n\tadd.s64 tb, %2, %18;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "}"
+      :: "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc), "n"(((1 & 3) * AS + (1 >> 2) * AH)), "n"(((1 & 3) * BS + (1 >> 2) * BH)),
+         "n"(((2 & 3) * AS + (2 >> 2) * AH)), "n"(((2 & 3) * BS + (2 >> 2) * BH)),
+         "n"(((3 & 3) * AS + (3 >> 2) * AH)), "n"(((3 & 3) * BS + (3 >> 2) * BH)),
+         "n"(((4 & 3) * AS + (4 >> 2) * AH)), "n"(((4 & 3) * BS + (4 >> 2) * BH)),
+         "n"(((5 & 3) * AS + (5 >> 2) * AH)), "n"(((5 & 3) * BS + (5 >> 2) * BH)),
+         "n"(((6 & 3) * AS + (6 >> 2) * AH)), "n"(((6 & 3) * BS + (6 >> 2) * BH)),
+         "n"(((7 & 3) * AS + (7 >> 2) * AH)), "n"(((7 & 3) * BS + (7 >> 2) * BH))
+      : "memory");
+}
+
+// TS variant: A from TMEM, step kk at a_tmem + 8 kk (16 bf16 = 8 columns); B as above.
+template <int BS, int BH>
+__device__ __forceinline__ void umma_ts_k128(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred e, p;\n\t.reg .b32 ta;\n\t.reg .b64 tb;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "setp.eq.u32 p, 0, 0;\n\t"
+      "add.s32 ta, %1, 8;\n\tadd.s64 tb, %2, %5;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "add.s32 ta, %1, 16;\n\tadd.s64 tb, %2, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "add.s32 ta, %1, 24;\n\tadd.s64 tb, %2, %7;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "add.s32 ta, %1, 32;\n\tadd.s64 tb, %2, %8;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "add.s32 ta, %1, 40;\n\tadd.s64 tb, %2, %9;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "add.s32 ta, %1, 48;\n\tadd.s64 tb, %2, %10;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "add.s32 ta, %1, 56;\n\tadd.s64 tb, %2, %11;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "}"
+      :: "r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "n"(((1 & 3) * BS + (1 >> 2) * BH)), "n"(((2 & 3) * BS + (2 >> 2) * BH)), "n"(((3 & 3) * BS + (3 >> 2) * BH)), "n"(((4 & 3) * BS + (4 >> 2) * BH)), "n"(((5 & 3) * BS + (5 >> 2) * BH)), "n"(((6 & 3) * BS + (6 >> 2) * BH)), "n"(((7 & 3) * BS + (7 >> 2) * BH))
+      : "memory");
+}
+
 // Arrive on an mbarrier once every previously issued tcgen05 op of this thread completes.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -281,6 +374,17 @@ __device__ __forceinline__ void ffma2(float& y0, float& y1, float x0, float x1, 
       "mov.b64 {%0, %1}, x;\n\t}"
       : "=f"(y0), "=f"(y1)
       : "f"(x0), "f"(x1), "f"(a), "f"(b));
+}
+// (y0, y1) = (a0, a1) * (b0, b1) + c
+__device__ __forceinline__ void ffma2_v(float& y0, float& y1, float a0, float a1, float b0, float b1, float c) {
+  asm("{\n\t.reg .b64 a, b, c;\n\t"
+      "mov.b64 a, {%2, %3};\n\t"
+      "mov.b64 b, {%4, %5};\n\t"
+      "mov.b64 c, {%6, %6};\n\t"
+      "fma.rn.ftz.f32x2 a, a, b, c;\n\t"
+      "mov.b64 {%0, %1}, a;\n\t}"
+      : "=f"(y0), "=f"(y1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c));
 }
 __device__ __forceinline__ void fadd2(float& a0, float& a1, float b0, float b1) {
   asm("{\n\t.reg .b64 a, b;\n\t"
