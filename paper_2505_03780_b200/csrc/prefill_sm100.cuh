@@ -119,7 +119,8 @@ __device__ __forceinline__ void prefill_decode_item(int w, const PrefillKernelAr
 // per-element compare/select at all — predicated-off instructions still cost issue slots.
 template <int BN, bool MASKED, int EMU>
 __device__ __forceinline__ float softmax_pass2(uint32_t s_addr, float sl2, float nmu, int kv0, int lim) {
-  float ls0 = 0.f, ls1 = 0.f;
+  // four independent FADD2 accumulators: a single running sum is a 64-deep dependent chain
+  float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int c = 0; c < BN / 64; ++c) {
     uint32_t ra[32], rb[32];
@@ -150,38 +151,45 @@ __device__ __forceinline__ float softmax_pass2(uint32_t s_addr, float sl2, float
           if (col0 + i > lim) e0 = 0.f;
           if (col0 + i + 1 > lim) e1 = 0.f;
         }
-        fadd2(ls0, ls1, e0, e1);
+        const int acc = ((i >> 1) & 3) * 2;
+        fadd2(ls[acc], ls[acc + 1], e0, e1);
         pk[i >> 1] = pack_bf16x2(e0, e1);
       }
     }
     tmem_st16(s_addr + c * 32, pa);  // P overwrites S columns this thread has already read
     tmem_st16(s_addr + c * 32 + 16, pb);
   }
-  return ls0 + ls1;
+  fadd2(ls[0], ls[1], ls[2], ls[3]);
+  fadd2(ls[4], ls[5], ls[6], ls[7]);
+  fadd2(ls[0], ls[1], ls[4], ls[5]);
+  return ls[0] + ls[1];
 }
 
 template <int BN, bool MASKED>
 __device__ __forceinline__ float softmax_rowmax(uint32_t s_addr, int kv0, int lim) {
-  float mt = -INFINITY;
+  // four independent 3-input max chains (FMNMX3) instead of one 64-deep chain
+  float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
   for (int c = 0; c < BN / 64; ++c) {
     uint32_t ra[32], rb[32];
     tmem_ld32x2(s_addr + c * 64, s_addr + c * 64 + 32, ra, rb);
 #pragma unroll
     for (int i = 0; i < 32; i += 2) {
+      float a0 = __uint_as_float(ra[i]), a1 = __uint_as_float(ra[i + 1]);
+      float b0 = __uint_as_float(rb[i]), b1 = __uint_as_float(rb[i + 1]);
       if constexpr (MASKED) {
         const int ca = kv0 + c * 64 + i, cb = ca + 32;
-        mt = fmaxf(mt, fmaxf(ca > lim ? -INFINITY : __uint_as_float(ra[i]),
-                             ca + 1 > lim ? -INFINITY : __uint_as_float(ra[i + 1])));
-        mt = fmaxf(mt, fmaxf(cb > lim ? -INFINITY : __uint_as_float(rb[i]),
-                             cb + 1 > lim ? -INFINITY : __uint_as_float(rb[i + 1])));
-      } else {
-        mt = fmaxf(mt, fmaxf(__uint_as_float(ra[i]), __uint_as_float(ra[i + 1])));
-        mt = fmaxf(mt, fmaxf(__uint_as_float(rb[i]), __uint_as_float(rb[i + 1])));
+        if (ca > lim) a0 = -INFINITY;
+        if (ca + 1 > lim) a1 = -INFINITY;
+        if (cb > lim) b0 = -INFINITY;
+        if (cb + 1 > lim) b1 = -INFINITY;
       }
+      const int k = (i >> 1) & 1;
+      m[k] = fmaxf(m[k], fmaxf(a0, a1));
+      m[2 + k] = fmaxf(m[2 + k], fmaxf(b0, b1));
     }
   }
-  return mt;
+  return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
 }
 
 #ifdef B200_TRACE
