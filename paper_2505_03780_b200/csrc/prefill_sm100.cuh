@@ -57,12 +57,14 @@ struct PrefillCfg {
   static constexpr int KV_BYTES = BN * D * 2;  // one K or V tile
   static constexpr int HALF_Q = BM * 128;
   static constexpr int HALF_KV = BN * 128;
+  // Q is double-buffered when the ring leaves room: the next item's Q lands during this item
+  static constexpr int QBUF = (2 * NQ * Q_BYTES + (NSTAGE_CFG + 1) * 32768 <= 229376) ? 2 : 1;
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_KV = OFF_Q + NQ * Q_BYTES;
+  static constexpr int OFF_KV = OFF_Q + QBUF * NQ * Q_BYTES;
   static constexpr int OFF_ITEM = OFF_KV + NSLOT * KV_BYTES;  // int32[2] work-item mailbox
   static constexpr int OFF_BAR = OFF_ITEM + 16;
-  // q_full, q_empty, kv_full/empty[NSLOT], s_full[NQ], p_full[NQ], o_full, o_free[NQ], item_full/empty[2]
-  static constexpr int NUM_BARS = 2 + 2 * NSLOT + 3 * NQ + 1 + 4;
+  // q_full[2], q_empty[2], kv_full/empty[NSLOT], s_full[NQ], p_full[NQ], o_full, o_free[NQ], item_full/empty[2]
+  static constexpr int NUM_BARS = 4 + 2 * NSLOT + 3 * NQ + 1 + 4;
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
   static constexpr uint32_t TMEM_COLS = 512;
   __host__ __device__ static constexpr uint32_t S_COL(int t) { return t * 128; }
@@ -218,9 +220,9 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
   uint8_t* sKV = smem + C::OFF_KV;
   volatile int32_t* item_box = reinterpret_cast<volatile int32_t*>(smem + C::OFF_ITEM);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* q_full = bars;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* kv_full = bars + 2;
+  uint64_t* q_full = bars;       // [2]
+  uint64_t* q_empty = bars + 2;  // [2]
+  uint64_t* kv_full = bars + 4;
   uint64_t* kv_empty = kv_full + NS;
   uint64_t* s_full = kv_empty + NS;   // [NQ]
   uint64_t* p_full = s_full + NQ;     // [NQ]
@@ -234,8 +236,10 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
   const int lane = lane_id();
 
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
     for (int i = 0; i < NS; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
@@ -285,11 +289,13 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
         const int seq_len = args.cu_seqlens[seq + 1] - seq_start;
         const int h0 = hg * NQ, kvh = h0 / args.group;
         const int n_kv = n_kv_of(seq_len, qblk);
-        mbar_wait(q_empty, (k & 1) ^ 1);
-        mbar_arrive_expect_tx(q_full, NQ * C::Q_BYTES);
+        const int qb = (C::QBUF == 2) ? (k & 1) : 0;
+        const uint32_t qph = (C::QBUF == 2) ? ((k >> 1) & 1) : (k & 1);
+        mbar_wait(&q_empty[qb], qph ^ 1);
+        mbar_arrive_expect_tx(&q_full[qb], NQ * C::Q_BYTES);
         for (int t = 0; t < NQ; ++t)
           for (int hf = 0; hf < 2; ++hf)
-            tma_load_3d(sQ + t * C::Q_BYTES + hf * C::HALF_Q, &tmap_q, q_full, hf * 64, h0 + t,
+            tma_load_3d(sQ + (qb * NQ + t) * C::Q_BYTES + hf * C::HALF_Q, &tmap_q, &q_full[qb], hf * 64, h0 + t,
                         seq_start + qblk * BM);
         for (int idx = 0; idx < 2 * n_kv; ++idx, ++ri) {
           const int slot = ri % NS;
@@ -314,8 +320,9 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
       const uint64_t q_desc = sdesc_sw128(smem_u32(sQ), 16, 1024);
       const uint64_t k_desc = sdesc_sw128(smem_u32(sKV), 16, 1024);
       const uint64_t v_desc = sdesc_sw128(smem_u32(sKV), C::HALF_KV, 1024);
+      int qb = 0;
       auto issue_qk = [&](int t, int slot) {
-        const uint64_t qa = q_desc + ((t * C::Q_BYTES) >> 4);
+        const uint64_t qa = q_desc + (((qb * NQ + t) * C::Q_BYTES) >> 4);
         const uint64_t kb = k_desc + ((slot * C::KV_BYTES) >> 4);
         umma_ss_k128<2, C::HALF_Q / 16, 2, C::HALF_KV / 16>(tmem + C::S_COL(t), qa, kb, IDESC_QK, 0u);
       };
@@ -341,7 +348,8 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
         prefill_decode_item(w, args, seq, qblk, hg);
         const int seq_start = args.cu_seqlens[seq];
         const int n_kv = n_kv_of(args.cu_seqlens[seq + 1] - seq_start, qblk);
-        mbar_wait(q_full, k & 1);
+        qb = (C::QBUF == 2) ? (k & 1) : 0;
+        mbar_wait(&q_full[qb], (C::QBUF == 2) ? ((k >> 1) & 1) : (k & 1));
         {
           const int slot = ri % NS;
           mbar_wait(&kv_full[slot], (ri / NS) & 1);
@@ -351,7 +359,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
             umma_commit_w(&s_full[t]);
           }
           umma_commit_w(&kv_empty[slot]);
-          if (n_kv == 1) umma_commit_w(q_empty);
+          if (n_kv == 1) umma_commit_w(&q_empty[qb]);
           ++ri;
         }
         for (int j = 0; j < n_kv; ++j) {
@@ -378,7 +386,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
               umma_commit_w(&s_full[t]);
               if (t == NQ - 1) {
                 umma_commit_w(&kv_empty[kslot]);
-                if (j + 2 == n_kv) umma_commit_w(q_empty);
+                if (j + 2 == n_kv) umma_commit_w(&q_empty[qb]);
               }
             }
           }
