@@ -67,7 +67,8 @@ typedef struct {
   int32_t head_dim;           /* 128 */
   int32_t causal;             /* 1: key j attends iff j <= query position (q_len == k_len) */
   float softmax_scale;        /* <= 0 -> 1/sqrt(head_dim) */
-  void* workspace;            /* longest-first work list; b200attn_prefill_workspace_size bytes */
+  void* workspace;            /* longest-first work list; b200attn_prefill_workspace_size bytes,
+                                 ZERO-FILLED once at allocation (the kernels keep its counter at 0) */
   size_t workspace_bytes;
 } b200attn_prefill_params;
 

@@ -116,7 +116,7 @@ def _workspace(device, nbytes: int, kind: str = "decode") -> Optional[torch.Tens
     key = (device.type, device.index, kind)
     buf = _workspaces.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)  # prefill counter must start at 0
         _workspaces[key] = buf
     return buf
 
@@ -276,7 +276,7 @@ class PrefillPlan:
             num_q_heads=q.shape[1], num_kv_heads=k.shape[1], head_dim=q.shape[2], causal=causal))
         self.var = prefill_variant(self.config)
         self.p = _prefill_params(q, k, v, self.out, cu_seqlens, max_seqlen, softmax_scale, causal, None)
-        self.ws = torch.empty(max(1, self.lib.b200attn_prefill_workspace_size(self.p)), dtype=torch.uint8,
+        self.ws = torch.zeros(max(1, self.lib.b200attn_prefill_workspace_size(self.p)), dtype=torch.uint8,
                               device=q.device)
         self.p.workspace, self.p.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
         self.device = q.device

@@ -117,9 +117,15 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   int nkeys = 0;
   prefill_ws_ints(p, &nkeys);
   int32_t* ws = reinterpret_cast<int32_t*>(p->workspace);
-  b200::prefill_schedule_kernel<<<1, 1024, 0, stream>>>(p->cu_seqlens, p->num_seqs, p->causal, nkeys, ws);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "prefill schedule launch");
+  // one sequence: its q blocks in reverse are already longest-first, so no schedule kernel; the
+  // kernel's last CTA re-zeroes the work counter (the workspace starts zeroed, see header)
+  const bool single = (p->num_seqs == 1);
+  cudaError_t e;
+  if (!single) {
+    b200::prefill_schedule_kernel<<<1, 1024, 0, stream>>>(p->cu_seqlens, p->num_seqs, p->causal, nkeys, ws);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "prefill schedule launch");
+  }
   b200::PrefillKernelArgs a;
   a.cu_seqlens = p->cu_seqlens;
   a.items = ws + 2 + nkeys;
@@ -131,6 +137,7 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   a.group = p->num_q_heads / p->num_kv_heads;
   a.causal = p->causal;
   a.num_hg = p->num_q_heads / NQ;
+  a.single_nqb = single ? (p->max_seqlen + C::BM - 1) / C::BM : 0;
   const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / sqrtf((float)p->head_dim);
   a.scale_log2 = scale * 1.4426950408889634f;
   // persistent: never more CTAs than work items (upper bound without a device read)

@@ -41,6 +41,8 @@ struct PrefillKernelArgs {
   int32_t group;  // Hq / Hkv
   int32_t causal;
   int32_t num_hg;    // Hq / NQ head groups per (seq, q block)
+  int32_t single_nqb;  // > 0: one sequence with this many q blocks -> no schedule kernel, items are
+                       // q blocks longest first; the work counter is then reset by the last CTA
   float scale_log2;  // softmax_scale * log2(e)
 };
 
@@ -111,6 +113,11 @@ __device__ __forceinline__ void prefill_decode_item(int w, const PrefillKernelAr
                                                     int& hg) {
   const int pair = w / a.num_hg;
   hg = w - pair * a.num_hg;
+  if (a.single_nqb > 0) {
+    seq = 0;
+    qblk = a.single_nqb - 1 - pair;
+    return;
+  }
   const int it = a.items[pair];
   seq = it >> 16;
   qblk = it & 0xFFFF;
@@ -273,7 +280,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
       tma_prefetch_desc(&tmap_q);
       tma_prefetch_desc(&tmap_k);
       tma_prefetch_desc(&tmap_v);
-      const int total_work = args.sched[1] * args.num_hg;
+      const int total_work = (args.single_nqb > 0 ? args.single_nqb : args.sched[1]) * args.num_hg;
       const uint64_t keep = policy_evict_last();  // K/V tiles are re-read by other q blocks / heads
       int ri = 0;
       for (int k = 0;; ++k) {
@@ -502,6 +509,15 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
     __syncwarp();
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+  if (args.single_nqb > 0 && threadIdx.x == 0) {
+    // every CTA has drawn its final (out-of-range) item before getting here
+    __threadfence();
+    if (atomicAdd(args.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      args.sched[0] = 0;
+      args.sched[1] = 0;
+      __threadfence();
+    }
   }
 }
 
