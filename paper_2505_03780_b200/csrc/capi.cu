@@ -89,7 +89,7 @@ size_t prefill_ws_ints(const b200attn_prefill_params* p, int* nkeys_out) {
   const int nkeys = (p->max_seqlen + 127) / 128;
   const size_t pairs = (size_t)p->total_tokens / 128 + (size_t)p->num_seqs + 1;
   if (nkeys_out) *nkeys_out = nkeys;
-  return 2 + (size_t)nkeys + pairs;
+  return 3 + (size_t)nkeys + pairs;
 }
 
 template <int NQ, int BN, int NS>
@@ -128,7 +128,7 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   }
   b200::PrefillKernelArgs a;
   a.cu_seqlens = p->cu_seqlens;
-  a.items = ws + 2 + nkeys;
+  a.items = ws + 3 + nkeys;
   a.sched = ws;
   a.o = reinterpret_cast<__nv_bfloat16*>(p->o);
   a.lse = p->lse;

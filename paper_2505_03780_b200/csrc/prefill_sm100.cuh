@@ -33,7 +33,7 @@ namespace b200 {
 struct PrefillKernelArgs {
   const int32_t* cu_seqlens;
   const int32_t* items;  // [n_pairs] (seq << 16) | q block, longest first
-  int32_t* sched;        // [0] = work counter (atomic), [1] = n_pairs
+  int32_t* sched;        // [0] = work counter (atomic), [1] = n_pairs, [2] = CTAs done
   __nv_bfloat16* o;
   float* lse;  // optional [Hq, T]
   int32_t total_tokens;
@@ -510,12 +510,13 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
   }
-  if (args.single_nqb > 0 && threadIdx.x == 0) {
-    // every CTA has drawn its final (out-of-range) item before getting here
+  if (threadIdx.x == 0) {
+    // every CTA has drawn its final (out-of-range) item before getting here: the last one out
+    // re-zeroes the work counter (sched[0]) and the done counter (sched[2]) for the next launch
     __threadfence();
-    if (atomicAdd(args.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+    if (atomicAdd(args.sched + 2, 1) == static_cast<int>(gridDim.x) - 1) {
       args.sched[0] = 0;
-      args.sched[1] = 0;
+      args.sched[2] = 0;
       __threadfence();
     }
   }
@@ -523,11 +524,11 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
 
 // Longest-first work list: one (seq, q block) entry per 128-row query block, sorted by causal
 // cost (q block index; non-causal: the sequence's block count) descending via a counting sort.
-// ws layout: [0] work counter, [1] n_pairs, [2 .. 2+nkeys) key offsets, then the items.
+// ws layout: [0] work counter, [1] n_pairs, [2] done counter, [3 .. 3+nkeys) key offsets, then items.
 __global__ void __launch_bounds__(1024) prefill_schedule_kernel(const int32_t* __restrict__ cu, int num_seqs,
                                                                 int causal, int nkeys, int32_t* __restrict__ ws) {
-  int32_t* hist = ws + 2;
-  int32_t* items = ws + 2 + nkeys;
+  int32_t* hist = ws + 3;
+  int32_t* items = ws + 3 + nkeys;
   __shared__ int32_t part[1024];
   const int tid = threadIdx.x;
   for (int k = tid; k < nkeys; k += 1024) hist[k] = 0;
