@@ -116,15 +116,9 @@ def barrier(world):
 
 
 def max_over_ranks(x: float, world: int) -> float:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
+    from paper_2505_03780_b200.parallel import max_over_ranks as _max
 
-    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return _max(x)
 
 
 def cuda_time(fn, reps: int, stream) -> float:
@@ -351,7 +345,9 @@ def run_b200(args, world, rank, local):
     sampler.join()
     ms = ev0.elapsed_time(ev1)
     ms_max = max_over_ranks(ms, world)
-    value = world * units * args.steps / (ms_max / 1e3) / scale
+    from paper_2505_03780_b200.parallel import weak_scaling_value
+
+    value = weak_scaling_value(units, args.steps, ms_max, world, scale)
 
     # ------------------------------------------------------------------ dominant kernel roofline
     if args.workload == "decode":
