@@ -31,7 +31,14 @@
 extern "C" {
 #endif
 
-#define B200ATTN_ABI_VERSION 1
+#define B200ATTN_ABI_VERSION 2 /* 2: kv_dtype / k_scale / v_scale appended to b200attn_decode_params,
+                                   b200attn_cache_append_fp8 added */
+
+/* KV-cache element type of b200attn_decode_params.kv_dtype */
+#define B200ATTN_KV_BF16 0
+#define B200ATTN_KV_FP8_E4M3 1 /* OCP e4m3 bytes, dequantised as x * k_scale (K) / x * v_scale (V):
+                                  vLLM's FP8_PER_TENSOR mode, the paper kernel family's upstream home
+                                  (vllm/v1/attention/ops/triton_unified_attention.py _cast_kv_tile) */
 
 typedef enum {
   B200ATTN_OK = 0,
@@ -76,12 +83,12 @@ typedef struct {
 typedef struct {
   int32_t num_splits; /* split-KV factor; 0 = heuristic (fill 148 SMs)                        */
   int32_t num_stages; /* depth of the K/V page-gather ring (32-KB slots)                      */
-  int32_t tile_n;     /* tokens per MMA tile: 128                                             */
+  int32_t tile_n;     /* tokens per MMA tile: 128 (per kv head) | 16 (page of all 8 kv heads)  */
 } b200attn_decode_variant;
 
 typedef struct {
   const void* q;              /* [batch, num_q_heads, head_dim] bf16                 */
-  const void* k_cache;        /* [num_blocks, block_size, num_kv_heads, head_dim] bf16 */
+  const void* k_cache;        /* [num_blocks, block_size, num_kv_heads, head_dim] bf16 (or e4m3, kv_dtype) */
   const void* v_cache;        /* same                                                */
   const int32_t* block_table; /* [batch, max_blocks_per_seq]                         */
   const int32_t* seq_lens;    /* [batch] cached tokens incl. the current one         */
@@ -97,6 +104,9 @@ typedef struct {
   int32_t max_blocks_per_seq;
   int32_t max_seq_len;        /* upper bound of seq_lens (sizes the split grid) */
   float softmax_scale;
+  int32_t kv_dtype;           /* B200ATTN_KV_BF16 | B200ATTN_KV_FP8_E4M3 (fp8: tile_n 16 variants only) */
+  float k_scale;              /* fp8 dequant scales (ignored for bf16); <= 0 -> 1 */
+  float v_scale;
 } b200attn_decode_params;
 
 int b200attn_abi_version(void);
@@ -133,6 +143,12 @@ int b200attn_combine(const float* part_o, const float* part_ml, void* o, int32_t
 int b200attn_cache_append(const void* new_k, const void* new_v, void* k_cache, void* v_cache,
                           const int64_t* slot_mapping, int32_t num_tokens, int32_t num_kv_heads,
                           int32_t head_dim, int32_t block_size, int32_t num_blocks, void* stream);
+
+/* Same for an fp8 e4m3 cache: new_k/new_v bf16 are quantised as satfinite_rn(x / k_scale) (resp. v_scale). */
+int b200attn_cache_append_fp8(const void* new_k, const void* new_v, void* k_cache, void* v_cache,
+                              const int64_t* slot_mapping, int32_t num_tokens, int32_t num_kv_heads,
+                              int32_t head_dim, int32_t block_size, int32_t num_blocks, float k_scale, float v_scale,
+                              void* stream);
 
 /* Descriptor self-test of the tcgen05 path (one CTA, no TMA):
  *   mode 0: D[128x128]  = A[128x128] . B[128x128]^T   A, B K-major

@@ -154,5 +154,80 @@ def decode_np(q, k_cache, v_cache, block_table, seq_lens, scale=None):
     return out
 
 
+# ----------------------------------------------------------------------------- fp8 (e4m3) KV cache
+def e4m3_table() -> np.ndarray:
+    """All 256 OCP FP8 E4M3 (``e4m3fn``) byte values as fp64: bias 7, no infinities, S.1111.111 = NaN,
+    exponent 0 = subnormal 2^-6 * m/8 (OCP 8-bit floating point specification v1.0, Table 1)."""
+    b = np.arange(256)
+    s = np.where(b >> 7, -1.0, 1.0)
+    e = (b >> 3) & 15
+    m = (b & 7).astype(np.float64)
+    v = np.where(e == 0, 2.0 ** -6 * m / 8, 2.0 ** (e - 7.0) * (1 + m / 8))
+    v = s * v
+    v[(e == 15) & ((b & 7) == 7)] = np.nan
+    return v
+
+
+_E4M3 = None
+
+
+def as_u8(x) -> np.ndarray:
+    if isinstance(x, np.ndarray):
+        assert x.dtype == np.uint8
+        return np.ascontiguousarray(x)
+    import torch
+
+    return x.detach().cpu().contiguous().view(torch.uint8).numpy()
+
+
+def decode_fp8_np(q, k_cache, v_cache, block_table, seq_lens, k_scale, v_scale, scale=None):
+    """Paged decode over an e4m3 cache: K = e4m3(k_cache) * k_scale, V = e4m3(v_cache) * v_scale
+    (vLLM FP8_PER_TENSOR: vllm/v1/attention/ops/triton_unified_attention.py _cast_kv_tile), the rest
+    exactly as ``decode_np``.  q bf16, caches uint8 [NB,bs,Hkv,D] -> O fp64 [B,Hq,D]."""
+    global _E4M3
+    if _E4M3 is None:
+        _E4M3 = e4m3_table()
+    qf = bf16_bits_to_f64(as_bf16_bits(q))
+    kc, vc = as_u8(k_cache), as_u8(v_cache)
+    bt, sl = _i32(block_table), _i32(seq_lens)
+    B, Hq, D = qf.shape
+    bs, Hkv = kc.shape[1], kc.shape[2]
+    G = Hq // Hkv
+    scale = float(scale) if scale else 1.0 / np.sqrt(D)
+    out = np.zeros_like(qf)
+    for b in range(B):
+        n = int(sl[b])
+        if n == 0:
+            continue
+        t = np.arange(n)
+        pages = bt[b, t // bs]
+        kk = np.repeat(_E4M3[kc[pages, t % bs]] * float(k_scale), G, axis=1)  # [n,Hq,D]
+        vv = np.repeat(_E4M3[vc[pages, t % bs]] * float(v_scale), G, axis=1)
+        sc = np.einsum("hd,nhd->hn", qf[b], kk) * scale
+        sc -= sc.max(-1, keepdims=True)
+        p = np.exp(sc)
+        p /= p.sum(-1, keepdims=True)
+        out[b] = np.einsum("hn,nhd->hd", p, vv)
+    return out
+
+
+def quantize_e4m3_np(x: np.ndarray, inv_scale: float) -> np.ndarray:
+    """fp64 -> e4m3 bytes, round-to-nearest-even on the value grid, saturating at +-448 (the
+    ``cvt.rn.satfinite.e4m3x2.f32`` semantics the cache-append kernel uses)."""
+    global _E4M3
+    if _E4M3 is None:
+        _E4M3 = e4m3_table()
+    y = np.clip(np.asarray(x, dtype=np.float64) * inv_scale, -448.0, 448.0)
+    pos = np.arange(0, 127)  # non-negative finite codes, ascending values
+    grid = _E4M3[pos]
+    mag = np.abs(y)
+    i = np.clip(np.searchsorted(grid, mag), 1, len(grid) - 1)
+    lo, hi = grid[i - 1], grid[i]
+    pick_hi = (mag - lo > hi - mag) | ((mag - lo == hi - mag) & (pos[i] % 2 == 0))
+    code = np.where(pick_hi, pos[i], pos[i - 1])
+    code = np.where(mag <= grid[0], 0, code)
+    return (code | np.where(np.signbit(y), 0x80, 0)).astype(np.uint8)  # -tiny -> -0, like cvt.rn
+
+
 if __name__ == "__main__":  # pragma: no cover
     print(build(force=bool(os.environ.get("FORCE"))))

@@ -45,7 +45,13 @@ class DecodeParams(ctypes.Structure):
     _fields_ = [("q", _P), ("k_cache", _P), ("v_cache", _P), ("block_table", _P), ("seq_lens", _P), ("o", _P),
                 ("workspace", _P), ("workspace_bytes", ctypes.c_size_t), ("batch", _I), ("num_q_heads", _I),
                 ("num_kv_heads", _I), ("head_dim", _I), ("block_size", _I), ("num_blocks", _I),
-                ("max_blocks_per_seq", _I), ("max_seq_len", _I), ("softmax_scale", ctypes.c_float)]
+                ("max_blocks_per_seq", _I), ("max_seq_len", _I), ("softmax_scale", ctypes.c_float),
+                ("kv_dtype", _I), ("k_scale", ctypes.c_float), ("v_scale", ctypes.c_float)]
+
+
+ABI_VERSION = 2
+KV_BF16 = 0
+KV_FP8_E4M3 = 1
 
 
 class B200AttnError(RuntimeError):
@@ -67,7 +73,7 @@ EXPORTS = (
     "b200attn_prefill_supported", "b200attn_decode_supported", "b200attn_prefill_workspace_size", "b200attn_prefill",
     "b200attn_decode_workspace_size", "b200attn_decode_num_splits", "b200attn_decode", "b200attn_decode_partial",
     "b200attn_combine",
-    "b200attn_cache_append", "b200attn_selftest_umma",
+    "b200attn_cache_append", "b200attn_cache_append_fp8", "b200attn_selftest_umma",
 )
 
 _lib = None
@@ -101,13 +107,16 @@ def load():
     lib.b200attn_decode_num_splits.argtypes = [DP, DV]
     lib.b200attn_combine.argtypes = [_P, _P, _P, _I, _I, _P]
     lib.b200attn_cache_append.argtypes = [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P]
+    lib.b200attn_cache_append_fp8.argtypes = [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, ctypes.c_float,
+                                              ctypes.c_float, _P]
     lib.b200attn_selftest_umma.argtypes = [ctypes.c_int, _P, _P, _P, _P]
     for name in ("b200attn_prefill_supported", "b200attn_decode_supported", "b200attn_prefill", "b200attn_decode",
                  "b200attn_decode_partial",
-                 "b200attn_combine", "b200attn_cache_append", "b200attn_selftest_umma", "b200attn_decode_num_splits"):
+                 "b200attn_combine", "b200attn_cache_append", "b200attn_cache_append_fp8", "b200attn_selftest_umma",
+                 "b200attn_decode_num_splits"):
         getattr(lib, name).restype = ctypes.c_int
-    if lib.b200attn_abi_version() != 1:
-        raise RuntimeError("libb200attn ABI mismatch")
+    if lib.b200attn_abi_version() != ABI_VERSION:
+        raise RuntimeError(f"libb200attn ABI {lib.b200attn_abi_version()} != {ABI_VERSION}; rebuild the library")
     _lib = lib
     return lib
 

@@ -121,20 +121,38 @@ def _workspace(device, nbytes: int, kind: str = "decode") -> Optional[torch.Tens
     return buf
 
 
-def _decode_params(q, k_cache, v_cache, block_table, seq_lens, out, max_seq_len, softmax_scale, ws=None, ws_bytes=0):
+FP8_DTYPE = torch.float8_e4m3fn  # OCP e4m3 KV cache (vLLM FP8_PER_TENSOR semantics)
+
+
+def _kv_dtype_code(cache: torch.Tensor) -> int:
+    if cache.dtype == torch.bfloat16:
+        return _native.KV_BF16
+    if cache.dtype == FP8_DTYPE:
+        return _native.KV_FP8_E4M3
+    raise TypeError(f"KV cache must be bfloat16 or float8_e4m3fn, got {cache.dtype}")
+
+
+def _check_cache(t: torch.Tensor, name: str):
+    _check(t, name, dtype=t.dtype if t.dtype in (torch.bfloat16, FP8_DTYPE) else torch.bfloat16, ndim=4)
+
+
+def _decode_params(q, k_cache, v_cache, block_table, seq_lens, out, max_seq_len, softmax_scale, ws=None, ws_bytes=0,
+                   k_scale=None, v_scale=None):
     B, Hq, D = q.shape
     NB, bs, Hkv, _ = k_cache.shape
     return _native.DecodeParams(
         _ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(block_table), _ptr(seq_lens), _ptr(out), _ptr(ws), ws_bytes, B,
-        Hq, Hkv, D, bs, NB, block_table.shape[1], int(max_seq_len), float(softmax_scale or 0.0))
+        Hq, Hkv, D, bs, NB, block_table.shape[1], int(max_seq_len), float(softmax_scale or 0.0),
+        _kv_dtype_code(k_cache), float(k_scale or 1.0), float(v_scale or 1.0))
 
 
-def decode_supported(q_shape, cache_shape, max_blocks_per_seq, max_seq_len, config: Mapping):
+def decode_supported(q_shape, cache_shape, max_blocks_per_seq, max_seq_len, config: Mapping, kv_dtype="bfloat16"):
     lib = _native.load()
     B, Hq, D = q_shape
     NB, bs, Hkv, _ = cache_shape
+    code = _native.KV_FP8_E4M3 if str(kv_dtype).startswith(("fp8", "float8")) else _native.KV_BF16
     p = _native.DecodeParams(None, None, None, None, None, None, None, 0, B, Hq, Hkv, D, bs, NB, max_blocks_per_seq,
-                             max_seq_len, 0.0)
+                             max_seq_len, 0.0, code, 1.0, 1.0)
     buf = _native.reason_buffer()
     rc = lib.b200attn_decode_supported(p, decode_variant(config), buf, len(buf))
     return rc, buf.value.decode()
@@ -142,15 +160,19 @@ def decode_supported(q_shape, cache_shape, max_blocks_per_seq, max_seq_len, conf
 
 def paged_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, block_table: torch.Tensor,
                  seq_lens: torch.Tensor, max_seq_len: Optional[int] = None, out: Optional[torch.Tensor] = None,
-                 softmax_scale: Optional[float] = None, config: Optional[Mapping] = None):
-    """Paged-KV decode: q [B,Hq,128]; caches [NB,bs,Hkv,128] bf16; block_table [B,maxblk] int32;
-    seq_lens [B] int32.  ``max_seq_len`` (host int) sizes the split grid; defaults to the
-    block-table capacity so no device->host sync is needed.
+                 softmax_scale: Optional[float] = None, config: Optional[Mapping] = None,
+                 k_scale: Optional[float] = None, v_scale: Optional[float] = None):
+    """Paged-KV decode: q [B,Hq,128]; caches [NB,bs,Hkv,128] bf16 or float8_e4m3fn (then K = k_cache * k_scale,
+    V = v_cache * v_scale, per-tensor); block_table [B,maxblk] int32; seq_lens [B] int32.
+    ``max_seq_len`` (host int) sizes the split grid; defaults to the block-table capacity so no
+    device->host sync is needed.
     """
     lib = _native.load()
     _check(q, "q", ndim=3)
-    _check(k_cache, "k_cache", ndim=4)
-    _check(v_cache, "v_cache", ndim=4)
+    _check_cache(k_cache, "k_cache")
+    _check_cache(v_cache, "v_cache")
+    if k_cache.dtype != v_cache.dtype:
+        raise TypeError("k_cache / v_cache dtype mismatch")
     _check(block_table, "block_table", dtype=torch.int32, ndim=2)
     _check(seq_lens, "seq_lens", dtype=torch.int32, ndim=1)
     if k_cache.shape != v_cache.shape:
@@ -164,9 +186,10 @@ def paged_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, 
     if config is None:
         config = default_decode_config(batch_size=q.shape[0], seq_len=int(max_seq_len), num_q_heads=q.shape[1],
                                        num_kv_heads=k_cache.shape[2], head_dim=q.shape[2],
-                                       block_size=k_cache.shape[1])
+                                       block_size=k_cache.shape[1], kv_dtype=_kv_name(k_cache))
     var = decode_variant(config)
-    p = _decode_params(q, k_cache, v_cache, block_table, seq_lens, out, max_seq_len, softmax_scale)
+    p = _decode_params(q, k_cache, v_cache, block_table, seq_lens, out, max_seq_len, softmax_scale,
+                       k_scale=k_scale, v_scale=v_scale)
     nbytes = lib.b200attn_decode_workspace_size(p, var)
     ws = _workspace(q.device, nbytes)
     if ws is not None:
@@ -181,7 +204,7 @@ def decode_num_splits(q_shape, cache_shape, max_blocks_per_seq, max_seq_len, con
     B, Hq, D = q_shape
     NB, bs, Hkv, _ = cache_shape
     p = _native.DecodeParams(None, None, None, None, None, None, None, 0, B, Hq, Hkv, D, bs, NB, max_blocks_per_seq,
-                             max_seq_len, 0.0)
+                             max_seq_len, 0.0, _native.KV_BF16, 1.0, 1.0)
     return int(lib.b200attn_decode_num_splits(p, decode_variant(config)))
 
 
@@ -197,19 +220,31 @@ def combine(part_o: torch.Tensor, part_ml: torch.Tensor, out: torch.Tensor):
     return out
 
 
+def _kv_name(cache: torch.Tensor) -> str:
+    return "fp8_e4m3" if cache.dtype == FP8_DTYPE else "bfloat16"
+
+
 def cache_append(new_k: torch.Tensor, new_v: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
-                 slot_mapping: torch.Tensor):
-    """Write new_k/new_v [N, Hkv, 128] into pages: slot = page * block_size + offset (int64, < 0 skips)."""
+                 slot_mapping: torch.Tensor, k_scale: Optional[float] = None, v_scale: Optional[float] = None):
+    """Write new_k/new_v [N, Hkv, 128] bf16 into pages: slot = page * block_size + offset (int64, < 0
+    skips).  float8_e4m3fn caches store satfinite_rn(x / k_scale) (resp. v_scale)."""
     lib = _native.load()
     _check(new_k, "new_k", ndim=3)
     _check(new_v, "new_v", ndim=3)
-    _check(k_cache, "k_cache", ndim=4)
-    _check(v_cache, "v_cache", ndim=4)
+    _check_cache(k_cache, "k_cache")
+    _check_cache(v_cache, "v_cache")
     _check(slot_mapping, "slot_mapping", dtype=torch.int64, ndim=1)
     NB, bs, Hkv, D = k_cache.shape
+    stream = torch.cuda.current_stream(new_k.device).cuda_stream
+    if _kv_dtype_code(k_cache) == _native.KV_FP8_E4M3:
+        if v_cache.dtype != FP8_DTYPE:
+            raise TypeError("k_cache / v_cache dtype mismatch")
+        _native.check(lib.b200attn_cache_append_fp8(_ptr(new_k), _ptr(new_v), _ptr(k_cache), _ptr(v_cache),
+                                                    _ptr(slot_mapping), new_k.shape[0], Hkv, D, bs, NB,
+                                                    float(k_scale or 1.0), float(v_scale or 1.0), stream))
+        return
     _native.check(lib.b200attn_cache_append(_ptr(new_k), _ptr(new_v), _ptr(k_cache), _ptr(v_cache),
-                                            _ptr(slot_mapping), new_k.shape[0], Hkv, D, bs, NB,
-                                            torch.cuda.current_stream(new_k.device).cuda_stream))
+                                            _ptr(slot_mapping), new_k.shape[0], Hkv, D, bs, NB, stream))
 
 
 def selftest_umma(mode: int, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
@@ -230,19 +265,21 @@ class DecodePlan:
     params struct and workspace, then ``run()`` is a single C-ABI call (K2 [+K3])."""
 
     def __init__(self, q, k_cache, v_cache, block_table, seq_lens, out=None, max_seq_len=None, config=None,
-                 softmax_scale=None):
+                 softmax_scale=None, k_scale=None, v_scale=None):
         self.lib = _native.load()
-        for t, n in ((q, "q"), (k_cache, "k_cache"), (v_cache, "v_cache")):
-            _check(t, n)
+        _check(q, "q")
+        _check_cache(k_cache, "k_cache")
+        _check_cache(v_cache, "v_cache")
         _check(block_table, "block_table", dtype=torch.int32, ndim=2)
         _check(seq_lens, "seq_lens", dtype=torch.int32, ndim=1)
         self.max_seq_len = int(max_seq_len if max_seq_len is not None else block_table.shape[1] * k_cache.shape[1])
         self.out = torch.empty_like(q) if out is None else out
         self.config = dict(config or default_decode_config(
             batch_size=q.shape[0], seq_len=self.max_seq_len, num_q_heads=q.shape[1], num_kv_heads=k_cache.shape[2],
-            head_dim=q.shape[2], block_size=k_cache.shape[1]))
+            head_dim=q.shape[2], block_size=k_cache.shape[1], kv_dtype=_kv_name(k_cache)))
         self.var = decode_variant(self.config)
-        self.p = _decode_params(q, k_cache, v_cache, block_table, seq_lens, self.out, self.max_seq_len, softmax_scale)
+        self.p = _decode_params(q, k_cache, v_cache, block_table, seq_lens, self.out, self.max_seq_len, softmax_scale,
+                                k_scale=k_scale, v_scale=v_scale)
         nbytes = self.lib.b200attn_decode_workspace_size(self.p, self.var)
         self.ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=q.device) if nbytes else None
         if self.ws is not None:

@@ -79,6 +79,23 @@ int make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint
   return B200ATTN_OK;
 }
 
+// 3-D byte map (fp8 pages) over [d2][d1][d0] with a {box0, box1, box2} unswizzled box.
+int make_map_u8_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
+                   uint64_t stride2_bytes, uint32_t box0, uint32_t box1, uint32_t box2) {
+  auto fn = encode_fn();
+  if (!fn) return fail(B200ATTN_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {box0, box1, box2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(B200ATTN_BAD_ARGS, "cuTensorMapEncodeTiled(u8) failed (%d)", static_cast<int>(r));
+  return B200ATTN_OK;
+}
+
 int num_sms();
 
 // ------------------------------------------------------------------ prefill variants
@@ -288,10 +305,10 @@ size_t flat_workspace_bytes(const b200attn_decode_params* p) {
 
 using FlatLauncher = int (*)(const b200attn_decode_params*, bool combine, cudaStream_t);
 
-template <int G, int NS>
+template <int G, int NS, bool FP8>
 int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stream) {
-  using C = b200::FlatCfg<G, NS>;
-  auto kern = b200::decode_flat_kernel<G, NS>;
+  using C = b200::FlatCfg<G, NS, FP8>;
+  auto kern = b200::decode_flat_kernel<G, NS, FP8>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -306,8 +323,13 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
     return rc;
   // head-major view of the page pool: dims {d, token, head}, strides {Hkv*D*2, D*2} (transposed)
   const uint64_t tokens = (uint64_t)p->num_blocks * p->block_size;
-  if ((rc = make_map_3d(&mk, p->k_cache, D, tokens, 8, 8ull * D * 2, D * 2ull, C::TT, 8))) return rc;
-  if ((rc = make_map_3d(&mv, p->v_cache, D, tokens, 8, 8ull * D * 2, D * 2ull, C::TT, 8))) return rc;
+  if (FP8) {  // one {128 d, 16 tokens, 8 heads} byte box = the whole 16-KB page
+    if ((rc = make_map_u8_3d(&mk, p->k_cache, D, tokens, 8, 8ull * D, D, D, C::TT, 8))) return rc;
+    if ((rc = make_map_u8_3d(&mv, p->v_cache, D, tokens, 8, 8ull * D, D, D, C::TT, 8))) return rc;
+  } else {
+    if ((rc = make_map_3d(&mk, p->k_cache, D, tokens, 8, 8ull * D * 2, D * 2ull, C::TT, 8))) return rc;
+    if ((rc = make_map_3d(&mv, p->v_cache, D, tokens, 8, 8ull * D * 2, D * 2ull, C::TT, 8))) return rc;
+  }
   const int ctas = num_sms();
   const size_t slots = (size_t)ctas + p->batch;
   b200::FlatDecodeArgs a;
@@ -322,6 +344,11 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
   a.max_blocks = p->max_blocks_per_seq;
   const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / sqrtf((float)p->head_dim);
   a.scale_log2 = scale * 1.4426950408889634f;
+  a.out_scale = 1.f;
+  if (FP8) {  // converted tiles hold x * 2^-8 (see e4m3x4_to_f16x4_s8)
+    a.scale_log2 *= (p->k_scale > 0.f ? p->k_scale : 1.f) * 256.f;
+    a.out_scale = (p->v_scale > 0.f ? p->v_scale : 1.f) * 256.f;
+  }
   kern<<<ctas, C::NTHREADS, C::SMEM_BYTES, stream>>>(mq, mk, mv, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "decode_flat launch");
@@ -336,13 +363,19 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
 
 struct FlatEntry {
   int g, ns;
+  bool fp8;
   FlatLauncher fn;
   int smem;
 };
-#define FF(G, NS) {G, NS, &launch_flat<G, NS>, b200::FlatCfg<G, NS>::SMEM_BYTES}
+#define FF(G, NS) {G, NS, false, &launch_flat<G, NS, false>, b200::FlatCfg<G, NS, false>::SMEM_BYTES}
+#define F8(G, NS) {G, NS, true, &launch_flat<G, NS, true>, b200::FlatCfg<G, NS, true>::SMEM_BYTES}
 const FlatEntry kFlat[] = {FF(1, 3), FF(1, 4), FF(1, 5), FF(1, 6), FF(2, 3), FF(2, 4), FF(2, 5), FF(2, 6),
-                           FF(4, 3), FF(4, 4), FF(4, 5), FF(8, 3), FF(8, 4)};
+                           FF(4, 3), FF(4, 4), FF(4, 5), FF(8, 3), FF(8, 4),
+                           // fp8 e4m3 KV: num_stages = depth of the 16-KB fp8 staging ring
+                           F8(1, 4), F8(1, 6), F8(2, 4), F8(2, 6), F8(4, 3), F8(4, 4), F8(4, 5), F8(8, 2),
+                           F8(8, 3)};
 #undef FF
+#undef F8
 
 int check_flat(const b200attn_decode_params* p, const b200attn_decode_variant* v, const FlatEntry** out) {
   if (v->num_splits != 0)
@@ -359,16 +392,18 @@ int check_flat(const b200attn_decode_params* p, const b200attn_decode_variant* v
     return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16 needs block_size >= 16, got %d", p->block_size);
   if (p->batch > b200::FlatCfg<1, 3>::MAXB)
     return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16 supports batch <= %d", b200::FlatCfg<1, 3>::MAXB);
+  const bool fp8 = p->kv_dtype == B200ATTN_KV_FP8_E4M3;
   const FlatEntry* e = nullptr;
   for (const auto& x : kFlat)
-    if (x.g == G && x.ns == v->num_stages) e = &x;
+    if (x.g == G && x.ns == v->num_stages && x.fp8 == fp8) e = &x;
   if (!e) {
     const int np = 8 * G < 16 ? 16 : 8 * G;
     const int est = v->num_stages * 32768 + 4 * np * 256 + 4096 + 1024;
     if (est > kMaxSmem)
       return fail(B200ATTN_SMEM_OVERFLOW, "TILE_N=16 num_stages=%d with %d q heads needs ~%d B smem > %d",
                   v->num_stages, p->num_q_heads, est, kMaxSmem);
-    return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16: no compiled variant for num_stages=%d", v->num_stages);
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16: no compiled %s variant for num_stages=%d with GQA %d",
+                fp8 ? "fp8" : "bf16", v->num_stages, G);
   }
   if (e->smem > kMaxSmem) return fail(B200ATTN_SMEM_OVERFLOW, "decode_flat smem %d B", e->smem);
   *out = e;
@@ -455,7 +490,11 @@ int resolve_decode(const b200attn_decode_params* p, const b200attn_decode_varian
   if (!p || !v) return fail(B200ATTN_BAD_ARGS, "null params/variant");
   int rc = check_decode_common(p);
   if (rc) return rc;
+  if (p->kv_dtype != B200ATTN_KV_BF16 && p->kv_dtype != B200ATTN_KV_FP8_E4M3)
+    return fail(B200ATTN_BAD_ARGS, "kv_dtype=%d", p->kv_dtype);
   if (v->tile_n == 16) return check_flat(p, v, &c->flat);
+  if (p->kv_dtype == B200ATTN_KV_FP8_E4M3)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "fp8 KV cache: compiled for TILE_N=16 (flat partition) only");
   return check_decode(p, v, &c->split);
 }
 
@@ -598,6 +637,26 @@ int b200attn_cache_append(const void* new_k, const void* new_v, void* k_cache, v
       (int64_t)num_blocks * block_size);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? B200ATTN_OK : cuda_fail(e, "cache_append launch");
+}
+
+int b200attn_cache_append_fp8(const void* new_k, const void* new_v, void* k_cache, void* v_cache,
+                              const int64_t* slot_mapping, int32_t num_tokens, int32_t num_kv_heads, int32_t head_dim,
+                              int32_t block_size, int32_t num_blocks, float k_scale, float v_scale, void* stream) {
+  g_err[0] = 0;
+  if (head_dim != 128) return fail(B200ATTN_UNSUPPORTED_CONFIG, "head_dim=%d (compiled for 128)", head_dim);
+  if (!new_k || !new_v || !k_cache || !v_cache || !slot_mapping || num_tokens < 0 || num_kv_heads <= 0)
+    return fail(B200ATTN_BAD_ARGS, "cache_append_fp8 args");
+  if (!(k_scale > 0.f) || !(v_scale > 0.f)) return fail(B200ATTN_BAD_ARGS, "k_scale / v_scale must be > 0");
+  if (num_tokens == 0) return B200ATTN_OK;
+  const long long rows = (long long)num_tokens * num_kv_heads;  // one 16-lane group per (token, head) row
+  const int threads = 256;
+  const long long blocks = (rows * 16 + threads - 1) / threads;
+  b200::cache_append_fp8_kernel<<<(unsigned)blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const uint4*>(new_k), reinterpret_cast<const uint4*>(new_v),
+      reinterpret_cast<uint2*>(k_cache), reinterpret_cast<uint2*>(v_cache), slot_mapping, num_tokens, num_kv_heads,
+      (int64_t)num_blocks * block_size, 1.f / k_scale, 1.f / v_scale);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? B200ATTN_OK : cuda_fail(e, "cache_append_fp8 launch");
 }
 
 #ifdef B200_TRACE

@@ -17,6 +17,13 @@
 // range may cover several sequences and parts of sequences; each (CTA, sequence) piece is a
 // segment: complete sequences are normalised and written by the CTA, pieces go to partial slot
 // (cta + seq) and K3' (flat_combine_kernel) merges them.
+//
+// FP8 = true (e4m3 KV cache, per-tensor k_scale / v_scale — vLLM's FP8_PER_TENSOR semantics):
+// TMA streams each 16-KB fp8 page into a staging ring (NSTAGE deep); four converter warps turn
+// it into an fp16 SW128 operand tile (exact, values x 2^-8; a 3-deep operand ring) and retype Q
+// bf16 -> fp16 in place; the MMAs run kind::f16 with fp16 P.  2^8 * k_scale is folded into the
+// softmax scale and 2^8 * v_scale into the output scale, so HBM traffic halves and nothing else
+// changes.
 #pragma once
 #include "sm100_common.cuh"
 
@@ -32,27 +39,32 @@ struct FlatDecodeArgs {
   int32_t batch;
   int32_t block_size;
   int32_t max_blocks;
-  float scale_log2;
+  float scale_log2;  // softmax_scale * log2(e)  (fp8: * k_scale * 2^8)
+  float out_scale;   // 1                        (fp8: v_scale * 2^8)
 };
 
-template <int G, int NSTAGE>
+template <int G, int NSTAGE, bool FP8 = false>
 struct FlatCfg {
   static constexpr int D = 128, HKV = 8, TT = 16, ROWS = 128;
   static constexpr int NQ = 8 * G;
   static constexpr int NP = NQ < 16 ? 16 : NQ;  // MMA N
-  static constexpr int NTHREADS = 192, TMA_WARP = 4, MMA_WARP = 5;
+  static constexpr int NTHREADS = FP8 ? 320 : 192, TMA_WARP = 4, MMA_WARP = 5, CONV_WARP0 = 6;
   static constexpr int SLOT = ROWS * D * 2, HALF = ROWS * 128;
+  static constexpr int OPS = FP8 ? 3 : NSTAGE;   // MMA operand ring (bf16 / fp16 tiles)
+  static constexpr int NSTG = FP8 ? NSTAGE : 0;  // fp8 staging ring (raw pages)
+  static constexpr int STG_SLOT = ROWS * D;      // one fp8 page of 8 kv heads x 16 tokens
   static constexpr int QB = NP * 256, QHALF = NP * 128;
   static constexpr int PB = NP * 256, PHALF = NP * 128;
   static constexpr int MAXB = 1024;
   static constexpr int OFF_KV = 0;
-  static constexpr int OFF_Q = OFF_KV + NSTAGE * SLOT;
+  static constexpr int OFF_STG = OFF_KV + OPS * SLOT;
+  static constexpr int OFF_Q = OFF_STG + NSTG * STG_SLOT;
   static constexpr int OFF_P = OFF_Q + 2 * QB;
   static constexpr int OFF_ALPHA = OFF_P + 2 * PB;     // [3][NP] f32
   static constexpr int OFF_ML = OFF_ALPHA + 3 * NP * 4;  // [2][NP] f32
   static constexpr int OFF_CU = OFF_ML + 2 * NP * 4;     // [MAXB + 1] i32
   static constexpr int OFF_BAR = (OFF_CU + (MAXB + 1) * 4 + 7) & ~7;
-  static constexpr int NUM_BARS = 4 + 2 * NSTAGE + 8;
+  static constexpr int NUM_BARS = 4 + 2 * OPS + 8 + 2 * NSTG + 2;
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
   static constexpr uint32_t TMEM_COLS = (4 * NP <= 64) ? 64 : (4 * NP <= 128 ? 128 : 256);
   __host__ __device__ static constexpr uint32_t S_COL(int i) { return (i & 1) * NP; }
@@ -63,15 +75,16 @@ __device__ __forceinline__ int flat_cta_of(int t, int ctas, int ntiles) {
   return static_cast<int>(((static_cast<long long>(t) + 1) * ctas - 1) / ntiles);
 }
 
-template <int G, int NSTAGE>
-__global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
+template <int G, int NSTAGE, bool FP8 = false>
+__global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
     decode_flat_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
                        const __grid_constant__ CUtensorMap tmap_v, const FlatDecodeArgs args) {
-  using C = FlatCfg<G, NSTAGE>;
-  constexpr int NQ = C::NQ, NP = C::NP, D = C::D;
+  using C = FlatCfg<G, NSTAGE, FP8>;
+  constexpr int NQ = C::NQ, NP = C::NP, D = C::D, OPS = C::OPS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sKV = smem + C::OFF_KV;
+  uint8_t* sSTG = smem + C::OFF_STG;
   uint8_t* sQ = smem + C::OFF_Q;
   uint8_t* sP = smem + C::OFF_P;
   float* alpha_s = reinterpret_cast<float*>(smem + C::OFF_ALPHA);
@@ -80,12 +93,15 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars;           // [2]
   uint64_t* q_empty = bars + 2;      // [2]
-  uint64_t* kv_full = bars + 4;      // [NSTAGE]
-  uint64_t* kv_empty = kv_full + NSTAGE;
-  uint64_t* s_full = kv_empty + NSTAGE;  // [2]
+  uint64_t* kv_full = bars + 4;      // [OPS] operand tile ready for the MMA
+  uint64_t* kv_empty = kv_full + OPS;
+  uint64_t* s_full = kv_empty + OPS;  // [2]
   uint64_t* p_full = s_full + 2;
   uint64_t* o_full = p_full + 2;
   uint64_t* o_empty = o_full + 2;
+  uint64_t* stg_full = o_empty + 2;  // [NSTG] fp8 page landed (FP8 only)
+  uint64_t* stg_empty = stg_full + C::NSTG;
+  uint64_t* q_conv = stg_empty + C::NSTG;  // [2] Q retyped to fp16 (FP8 only)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS);
   const int warp = warp_id(), lane = lane_id();
   const int B = args.batch;
@@ -114,9 +130,17 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
     mbar_init(&q_full[1], 1);
     mbar_init(&q_empty[0], 1);
     mbar_init(&q_empty[1], 1);
-    for (int i = 0; i < NSTAGE; ++i) {
-      mbar_init(&kv_full[i], 1);
+    for (int i = 0; i < OPS; ++i) {
+      mbar_init(&kv_full[i], FP8 ? 128 : 1);
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < C::NSTG; ++i) {
+      mbar_init(&stg_full[i], 1);
+      mbar_init(&stg_empty[i], 128);
+    }
+    if (FP8) {
+      mbar_init(&q_conv[0], 128);
+      mbar_init(&q_conv[1], 128);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
@@ -181,7 +205,16 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
           const int pg = __shfl_sync(0xffffffffu, page, j);
           const int tok = (base + j - tile0) * C::TT;
           const int row = pg * bs + (tok & (bs - 1));
-          if (lane == 0) {
+          if (FP8 && lane == 0) {
+#pragma unroll
+            for (int kv = 0; kv < 2; ++kv, ++it) {
+              const int slot = it % C::NSTG;
+              mbar_wait(&stg_empty[slot], ((it / C::NSTG) & 1) ^ 1);
+              mbar_arrive_expect_tx(&stg_full[slot], C::STG_SLOT);
+              tma_load_3d_hint(sSTG + slot * C::STG_SLOT, kv ? &tmap_v : &tmap_k, &stg_full[slot], 0, row, 0,
+                               stream_once);
+            }
+          } else if (lane == 0) {
 #pragma unroll
             for (int kv = 0; kv < 2; ++kv, ++it) {
               const int slot = it % NSTAGE;
@@ -200,15 +233,15 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
   } else if (warp == C::MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer (whole warp, one elected lane issues)
     {
-      constexpr uint32_t IDESC_QK = idesc_bf16_f32(C::ROWS, NP, false, false);
-      constexpr uint32_t IDESC_PV = idesc_bf16_f32(D, NP, true, false);
+      constexpr uint32_t IDESC_QK = FP8 ? idesc_f16_f32(C::ROWS, NP, false, false) : idesc_bf16_f32(C::ROWS, NP, false, false);
+      constexpr uint32_t IDESC_PV = FP8 ? idesc_f16_f32(D, NP, true, false) : idesc_bf16_f32(D, NP, true, false);
       const uint64_t k_desc = sdesc_sw128(smem_u32(sKV), 16, 1024);
       const uint64_t v_desc = sdesc_sw128(smem_u32(sKV), C::HALF, 1024);
       const uint64_t q_desc = sdesc_sw128(smem_u32(sQ), 16, 1024);
       const uint64_t p_desc = sdesc_sw128(smem_u32(sP), 16, 1024);
       auto qk = [&](int i, int qb) {
-        const int idx = 2 * i, slot = idx % NSTAGE;
-        mbar_wait(&kv_full[slot], (idx / NSTAGE) & 1);
+        const int idx = 2 * i, slot = idx % OPS;
+        mbar_wait(&kv_full[slot], (idx / OPS) & 1);
         tc_fence_after();
         const uint64_t kb = k_desc + ((slot * C::SLOT) >> 4), qa = q_desc + ((qb * C::QB) >> 4);
         umma_ss_k128<2, C::HALF / 16, 2, C::QHALF / 16>(tmem + C::S_COL(i), kb, qa, IDESC_QK, 0u);
@@ -216,8 +249,8 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
         umma_commit_w(&kv_empty[slot]);
       };
       auto pv = [&](int i) {
-        const int idx = 2 * i + 1, slot = idx % NSTAGE;
-        mbar_wait(&kv_full[slot], (idx / NSTAGE) & 1);
+        const int idx = 2 * i + 1, slot = idx % OPS;
+        mbar_wait(&kv_full[slot], (idx / OPS) & 1);
         mbar_wait(&p_full[i & 1], (i >> 1) & 1);
         if (i >= 2) mbar_wait(&o_empty[i & 1], ((i >> 1) - 1) & 1);
         tc_fence_after();
@@ -230,7 +263,7 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
       for (int t = T0; t < T1; ++k) {
         while (cu[b + 1] <= t) ++b;
         const int seg_end = min(T1, cu[b + 1]);
-        mbar_wait(&q_full[k & 1], (k >> 1) & 1);
+        mbar_wait(FP8 ? &q_conv[k & 1] : &q_full[k & 1], (k >> 1) & 1);
         for (; t < seg_end; ++t, ++i) {
           qk(i, k & 1);
           if (t == seg_end - 1) umma_commit_w(&q_empty[k & 1]);
@@ -238,6 +271,55 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
         }
       }
       pv(i - 1);
+    }
+  } else if (FP8 && warp >= C::CONV_WARP0) {
+    // ------------------------------------------------------------ fp8 -> fp16 converters (FP8 only)
+    const int ct = threadIdx.x - 32 * C::CONV_WARP0;
+    const uint32_t stg0 = smem_u32(sSTG), kv0 = smem_u32(sKV);
+    int it = 0, k = 0, b = b_first;
+    for (int t = T0; t < T1; ++k) {
+      while (cu[b + 1] <= t) ++b;
+      const int seg_end = min(T1, cu[b + 1]);
+      mbar_wait(&q_full[k & 1], (k >> 1) & 1);
+      uint32_t* qw = reinterpret_cast<uint32_t*>(sQ + (k & 1) * C::QB);
+      for (int x = ct; x < NQ * 64; x += 128) {  // rows >= NQ are zero padding (0 -> 0)
+        const int r = x >> 6, h = (x >> 5) & 1, w = x & 31;  // row, 64-col half, word in the 128-B line
+        qw[h * (C::QHALF / 4) + r * 32 + w] = bf16x2_to_f16x2(qw[h * (C::QHALF / 4) + r * 32 + w]);
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&q_conv[k & 1]);
+      for (; t < seg_end; ++t) {
+#pragma unroll 1
+        for (int kv = 0; kv < 2; ++kv, ++it) {
+          const int slot = it % C::NSTG, oslot = it % OPS;
+          mbar_wait(&stg_full[slot], (it / C::NSTG) & 1);
+          mbar_wait(&kv_empty[oslot], ((it / OPS) & 1) ^ 1);
+          const uint32_t src = stg0 + slot * C::STG_SLOT, dst = kv0 + oslot * C::SLOT;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int id = j * 128 + ct, row = id >> 3, c = id & 7;  // row = head*16 + token, 16 d per chunk
+            const uint4 w = ld_shared_v4(src + row * 128 + c * 16);
+            uint32_t f[8];
+            e4m3x4_to_f16x4_s8(w.x, f[0], f[1]);
+            e4m3x4_to_f16x4_s8(w.y, f[2], f[3]);
+            e4m3x4_to_f16x4_s8(w.z, f[4], f[5]);
+            e4m3x4_to_f16x4_s8(w.w, f[6], f[7]);
+            // d [16c, 16c+16) -> 64-col half c/4, 16-B chunks 2(c%4) and 2(c%4)+1, SW128 (chunk ^ row%8)
+            const uint32_t line = dst + (c >> 2) * C::HALF + row * 128;
+            const int x0 = (2 * c) & 7, sw = row & 7;
+            if (c < 4) {  // even chunks first for c < 4, odd first for c >= 4: no bank conflicts
+              st_shared_v4(line + ((x0 ^ sw) << 4), f[0], f[1], f[2], f[3]);
+              st_shared_v4(line + (((x0 + 1) ^ sw) << 4), f[4], f[5], f[6], f[7]);
+            } else {
+              st_shared_v4(line + (((x0 + 1) ^ sw) << 4), f[4], f[5], f[6], f[7]);
+              st_shared_v4(line + ((x0 ^ sw) << 4), f[0], f[1], f[2], f[3]);
+            }
+          }
+          mbar_arrive(&stg_empty[slot]);
+          fence_proxy_async_smem();
+          mbar_arrive(&kv_full[oslot]);
+        }
+      }
     }
   } else {
     // ------------------------------------------------------------ softmax / fold / epilogue
@@ -302,17 +384,24 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
           l_part[g] = fmaf(l_part[g], alpha[g], p);
           m_run[g] = mn;
           const int qh = h * G + g;
-          const __nv_bfloat16 pv16 = __float2bfloat16_rn(p);
-          asm volatile("st.shared.b16 [%0], %1;" ::"r"(pb + qh * 128 + ((rchunk ^ (qh & 7)) << 4)),
-                       "h"(*reinterpret_cast<const uint16_t*>(&pv16))
+          uint16_t pbits;
+          if constexpr (FP8) {
+            const __half p16 = __float2half_rn(p);
+            pbits = *reinterpret_cast<const uint16_t*>(&p16);
+          } else {
+            const __nv_bfloat16 p16 = __float2bfloat16_rn(p);
+            pbits = *reinterpret_cast<const uint16_t*>(&p16);
+          }
+          asm volatile("st.shared.b16 [%0], %1;" ::"r"(pb + qh * 128 + ((rchunk ^ (qh & 7)) << 4)), "h"(pbits)
                        : "memory");
           if (t16 == 0) alpha_s[(i % 3) * NP + qh] = alpha[g];
         }
-        if (!valid) {
+        if (!FP8 && !valid) {
           // the page's tail slots past the sequence end hold arbitrary bytes: P = 0 there, but
-          // 0 * NaN would poison O, so zero this row of the V tile before PV reads it
-          const int vidx = 2 * i + 1, vslot = vidx % NSTAGE;
-          mbar_wait(&kv_full[vslot], (vidx / NSTAGE) & 1);
+          // 0 * NaN would poison O, so zero this row of the V tile before PV reads it (the fp8
+          // conversion cannot produce NaN/Inf, so the FP8 path needs no zeroing)
+          const int vidx = 2 * i + 1, vslot = vidx % OPS;
+          mbar_wait(&kv_full[vslot], (vidx / OPS) & 1);
           uint4* vr = reinterpret_cast<uint4*>(sKV + vslot * C::SLOT + row * 128);
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
@@ -344,12 +433,13 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE>::NTHREADS, 1)
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
           const float l = ml_s[NP + q];
-          args.o[(static_cast<size_t>(b) * NQ + q) * D + row] = __float2bfloat16_rn(l > 0.f ? o_acc[q] / l : 0.f);
+          args.o[(static_cast<size_t>(b) * NQ + q) * D + row] =
+              __float2bfloat16_rn(l > 0.f ? o_acc[q] * args.out_scale / l : 0.f);
         }
       } else {
         const size_t slot = static_cast<size_t>(blockIdx.x) + b;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) args.part_o[(slot * NQ + q) * D + row] = o_acc[q];
+        for (int q = 0; q < NQ; ++q) args.part_o[(slot * NQ + q) * D + row] = o_acc[q] * args.out_scale;
         if (row < NQ) {
           args.part_ml[(slot * NQ + row) * 2 + 0] = ml_s[row];
           args.part_ml[(slot * NQ + row) * 2 + 1] = ml_s[NP + row];

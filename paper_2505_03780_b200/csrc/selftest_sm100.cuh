@@ -120,6 +120,36 @@ __global__ void cache_append_kernel(const uint4* __restrict__ nk, const uint4* _
   else vc[dst + lane - 16] = nv[src + lane - 16];
 }
 
+// fp8 variant: 16 lanes per (token, kv head) row, 8 bf16 -> 8 e4m3 each (satfinite, RN), K and V.
+__device__ __forceinline__ uint32_t f32x4_to_e4m3x4(float a, float b, float c, float d) {
+  uint16_t lo, hi;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(b), "f"(a));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(d), "f"(c));
+  return static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+}
+
+__device__ __forceinline__ uint2 bf16x8_to_e4m3x8(uint4 x, float inv) {
+  auto f = [&](uint32_t w, int hi) { return __uint_as_float(hi ? (w & 0xFFFF0000u) : (w << 16)) * inv; };
+  return make_uint2(f32x4_to_e4m3x4(f(x.x, 0), f(x.x, 1), f(x.y, 0), f(x.y, 1)),
+                    f32x4_to_e4m3x4(f(x.z, 0), f(x.z, 1), f(x.w, 0), f(x.w, 1)));
+}
+
+__global__ void cache_append_fp8_kernel(const uint4* __restrict__ nk, const uint4* __restrict__ nv,
+                                        uint2* __restrict__ kc, uint2* __restrict__ vc,
+                                        const int64_t* __restrict__ slots, int num_tokens, int kv_heads,
+                                        int64_t num_slots, float inv_k, float inv_v) {
+  const long long g = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 4;
+  const int l = threadIdx.x & 15;
+  if (g >= static_cast<long long>(num_tokens) * kv_heads) return;
+  const int tok = static_cast<int>(g / kv_heads), h = static_cast<int>(g % kv_heads);
+  const int64_t slot = slots[tok];
+  if (slot < 0 || slot >= num_slots) return;
+  const int64_t src = (static_cast<int64_t>(tok) * kv_heads + h) * 16 + l;  // 8 bf16 per lane
+  const int64_t dst = (slot * kv_heads + h) * 16 + l;                       // 8 fp8 per lane
+  kc[dst] = bf16x8_to_e4m3x8(nk[src], inv_k);
+  vc[dst] = bf16x8_to_e4m3x8(nv[src], inv_v);
+}
+
 }  // namespace b200
 
 namespace b200 {

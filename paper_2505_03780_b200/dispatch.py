@@ -28,7 +28,9 @@ PREFILL_FIXED_BASELINE = {"BLOCK_M": 128, "BLOCK_N": 128, "num_warps": 4, "num_s
 DECODE_DEFAULT = {"num_splits": 0, "num_stages": 5, "TILE_N": 16}  # flat partition, 8 kv heads per tile
 DECODE_SPLIT_DEFAULT = {"num_splits": 0, "num_stages": 4, "TILE_N": 128}  # any geometry
 
-_GEOM = ("num_q_heads", "num_kv_heads", "head_dim", "block_size", "causal")
+_GEOM = ("num_q_heads", "num_kv_heads", "head_dim", "block_size", "causal", "kv_dtype")
+# fp8 KV (TILE_N=16 only): num_stages = fp8 staging-ring depth; deepest compiled variant per GQA group
+FP8_DECODE_STAGES = {1: 6, 2: 6, 4: 5, 8: 3}
 
 _table = None
 
@@ -79,6 +81,8 @@ def lookup(op: str, dims: dict) -> Optional[dict]:
     for shape, cfg in rows:
         if any(k in shape and k in dims and shape[k] != dims[k] for k in _GEOM):
             continue
+        if shape.get("kv_dtype", "bfloat16") != dims.get("kv_dtype", "bfloat16"):
+            continue
         d = 0.0
         for k in ("batch_size", "seq_len"):
             if k in shape and k in dims and shape[k] and dims[k]:
@@ -113,6 +117,12 @@ def flat_decode_ok(num_q_heads=32, num_kv_heads=8, block_size=16, batch_size=1, 
 
 
 def default_decode_config(**dims) -> dict:
+    if str(dims.get("kv_dtype", "bfloat16")).startswith(("fp8", "float8")):
+        cfg = lookup("decode", dims)
+        G = dims.get("num_q_heads", 32) // max(dims.get("num_kv_heads", 8), 1)
+        if cfg is None or cfg.get("TILE_N") != 16:
+            cfg = {"num_splits": 0, "num_stages": FP8_DECODE_STAGES.get(G, 4), "TILE_N": 16}
+        return dict(cfg)
     cfg = lookup("decode", dims)
     if cfg is None:
         cfg = DECODE_DEFAULT if flat_decode_ok(**dims) else DECODE_SPLIT_DEFAULT

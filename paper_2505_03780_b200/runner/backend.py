@@ -142,7 +142,8 @@ class B200Backend:
                                             config=config)
         out = torch.empty_like(x.q)
         return lambda: A.paged_decode(x.q, x.k_cache, x.v_cache, x.block_table, x.seq_lens,
-                                      max_seq_len=x.max_seq_len, out=out, config=config)
+                                      max_seq_len=x.max_seq_len, out=out, config=config, k_scale=x.k_scale,
+                                      v_scale=x.v_scale)
 
     def _precheck(self, config: dict, shape: dict):
         """Config/shape validity without allocating (C-ABI *_supported)."""
@@ -162,7 +163,8 @@ class B200Backend:
         else:
             B, ctx, bs = int(shape["batch_size"]), int(shape["seq_len"]), int(shape.get("block_size", 16))
             mb = (ctx + bs - 1) // bs
-            rc, why = A.decode_supported((B, Hq, D), (B * mb, bs, Hkv, D), mb, ctx, config)
+            rc, why = A.decode_supported((B, Hq, D), (B * mb, bs, Hkv, D), mb, ctx, config,
+                                         kv_dtype=shape.get("kv_dtype", "bfloat16"))
         if rc in _native.INVALID_CODES:
             return why
         if rc != _native.OK:

@@ -9,7 +9,9 @@ runner builds them here from the shape dims (SURVEY §8(d) conventions):
   prefill: {"op":"prefill","batch_size","seq_len" | "seq_len_min","seq_len_max","len_dist",
             "num_q_heads","num_kv_heads","head_dim","causal","dtype","seed"}
   decode:  {"op":"decode","batch_size","seq_len","num_q_heads","num_kv_heads","head_dim",
-            "block_size","dtype","seed"}
+            "block_size","dtype","seed"[,"kv_dtype":"fp8_e4m3"]}
+  fp8 caches hold e4m3(randn * FP8_INV_SCALE) and are read back with k_scale = v_scale =
+  1 / FP8_INV_SCALE (per-tensor, vLLM FP8_PER_TENSOR convention).
 
 Small tensors follow the reference exactly (CPU generator, fp32 randn -> bf16).  Tensors above
 ``CPU_GEN_LIMIT`` elements are drawn from a seeded CUDA generator instead (a 32-GiB paged cache
@@ -24,6 +26,7 @@ from typing import Optional
 import torch
 
 CPU_GEN_LIMIT = 1 << 26
+FP8_INV_SCALE = 64.0  # randn * 64 stays inside e4m3's +-448 for |x| < 7
 
 
 def varlen_lengths(shape: dict) -> list[int]:
@@ -41,22 +44,24 @@ def varlen_lengths(shape: dict) -> list[int]:
     raise ValueError(f"unknown len_dist {dist!r}")
 
 
-def _randn(shape, gen_kind: str, seed: int, device) -> torch.Tensor:
+def _randn(shape, gen_kind: str, seed: int, device, fp8: bool = False) -> torch.Tensor:
     n = 1
     for s in shape:
         n *= int(s)
     kind = gen_kind if gen_kind != "auto" else ("cpu" if n <= CPU_GEN_LIMIT else "cuda")
+    dt = torch.float8_e4m3fn if fp8 else torch.bfloat16
+    mul = FP8_INV_SCALE if fp8 else 1.0
     if kind == "cpu":
         g = torch.Generator(device="cpu").manual_seed(seed)
-        return torch.randn(shape, generator=g, dtype=torch.float32).to(torch.bfloat16).to(device)
+        return (torch.randn(shape, generator=g, dtype=torch.float32) * mul).to(dt).to(device)
     g = torch.Generator(device=device).manual_seed(seed)
-    out = torch.empty(shape, dtype=torch.bfloat16, device=device)
+    out = torch.empty(shape, dtype=dt, device=device)
     # fill in fp32 chunks to bound the temporary
     flat = out.view(-1)
     step = 1 << 27
     for i in range(0, n, step):
         m = min(step, n - i)
-        flat[i:i + m] = torch.randn(m, generator=g, dtype=torch.float32, device=device).to(torch.bfloat16)
+        flat[i:i + m] = (torch.randn(m, generator=g, dtype=torch.float32, device=device) * mul).to(dt)
     return out
 
 
@@ -87,12 +92,14 @@ class DecodeInputs:
     seq_lens: torch.Tensor
     max_seq_len: int
     lens: list
+    k_scale: Optional[float] = None
+    v_scale: Optional[float] = None
 
     @property
     def kv_bytes(self) -> int:
-        """K+V bytes the decode must read: 2 * sum(n) * Hkv * D * 2."""
+        """K+V bytes the decode must read: 2 * sum(n) * Hkv * D * elem (2 for bf16, 1 for fp8)."""
         Hkv, D = self.k_cache.shape[2], self.k_cache.shape[3]
-        return 2 * sum(self.lens) * Hkv * D * 2
+        return 2 * sum(self.lens) * Hkv * D * self.k_cache.element_size()
 
     @property
     def total_bytes(self) -> int:
@@ -125,12 +132,14 @@ def make_decode(shape: dict, device="cuda", gen: str = "auto", seed: Optional[in
     max_blocks = max(max_blocks, 1)
     NB = B * max_blocks + extra_blocks
     q = _randn((B, Hq, D), gen, seed, device)
-    kc = _randn((NB, bs, Hkv, D), gen, seed + 1, device)
-    vc = _randn((NB, bs, Hkv, D), gen, seed + 2, device)
+    fp8 = str(shape.get("kv_dtype", "bfloat16")).startswith(("fp8", "float8"))
+    kc = _randn((NB, bs, Hkv, D), gen, seed + 1, device, fp8=fp8)
+    vc = _randn((NB, bs, Hkv, D), gen, seed + 2, device, fp8=fp8)
     g = torch.Generator(device="cpu").manual_seed(seed + 3)
     perm = torch.randperm(NB, generator=g)[: B * max_blocks].to(torch.int32).reshape(B, max_blocks)
+    sc = 1.0 / FP8_INV_SCALE if fp8 else None
     return DecodeInputs(q, kc, vc, perm.to(device), torch.tensor(lens, dtype=torch.int32, device=device),
-                        max(lens) if lens else 0, lens)
+                        max(lens) if lens else 0, lens, sc, sc)
 
 
 # the BASELINE.json configurations

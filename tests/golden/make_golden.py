@@ -108,12 +108,48 @@ def decode_case(name, lens, Hq, Hkv, D=128, bs=16, seed=0):
     print(name, "B", B, "out|max|", float(out.abs().max()))
 
 
+def decode_fp8_case(name, lens, Hq, Hkv, D=128, bs=16, seed=0, k_scale=1 / 64, v_scale=1 / 32):
+    """fp8 e4m3 paged cache, per-tensor descales (vLLM KVQuantMode.FP8_PER_TENSOR)."""
+    from vllm.v1.attention.ops.triton_unified_attention import KVQuantMode, unified_attention
+
+    g = torch.Generator().manual_seed(seed)
+    B = len(lens)
+    nblk = [(L + bs - 1) // bs for L in lens]
+    NB = sum(nblk) + 3
+    q = bf16_inputs((B, Hq, D), g)
+    kc = (torch.randn((NB, bs, Hkv, D), generator=g) / k_scale).to(torch.float8_e4m3fn)
+    vc = (torch.randn((NB, bs, Hkv, D), generator=g) / v_scale).clamp(-448, 448).to(torch.float8_e4m3fn)
+    perm = torch.randperm(NB, generator=g)
+    bt = torch.zeros(B, max(nblk), dtype=torch.int32)
+    pi = 0
+    for b in range(B):
+        for j in range(nblk[b]):
+            bt[b, j] = int(perm[pi])
+            pi += 1
+    sl = torch.tensor(lens, dtype=torch.int32)
+    out = torch.zeros(B, Hq, D)
+    unified_attention(q.float(), kc, vc, out, torch.arange(B + 1, dtype=torch.int32), 1, sl, max(lens), D ** -0.5,
+                      True, (-1, -1), bt, 0, None, torch.tensor([k_scale]), torch.tensor([v_scale]),
+                      kv_quant_mode=KVQuantMode.FP8_PER_TENSOR)
+    u8 = lambda x: x.view(torch.uint8).numpy()  # noqa: E731
+    np.savez_compressed(OUT / f"{name}.npz", kind="decode_fp8", q=bits(q), k_cache=u8(kc), v_cache=u8(vc),
+                        block_table=bt.numpy(), seq_lens=sl.numpy(), k_scale=np.float64(k_scale),
+                        v_scale=np.float64(v_scale), out=out.numpy().astype(np.float32),
+                        source="vllm-0.22.0 triton_unified_attention FP8_PER_TENSOR (TRITON_INTERPRET=1, fp32 q "
+                        "storage of bf16 values)")
+    print(name, "B", B, "out|max|", float(out.abs().max()))
+
+
 def main():
+    if "--fp8" in sys.argv:  # only the fp8 fixture (the others are committed)
+        decode_fp8_case("decode_fp8_gqa4", [1, 33, 250, 16], Hq=32, Hkv=8, seed=6)
+        return
     prefill_case("prefill_varlen_gqa4", [1, 7, 64, 130], Hq=8, Hkv=2, seed=1)
     prefill_case("prefill_single_200_gqa4", [200], Hq=4, Hkv=1, seed=2)
     prefill_case("prefill_mha", [33, 129], Hq=2, Hkv=2, seed=3)
     decode_case("decode_ragged_gqa4", [1, 17, 200, 64], Hq=8, Hkv=2, seed=4)
     decode_case("decode_gqa8_bs32", [300, 45], Hq=16, Hkv=2, bs=32, seed=5)
+    decode_fp8_case("decode_fp8_gqa4", [1, 33, 250, 16], Hq=32, Hkv=8, seed=6)
 
 
 if __name__ == "__main__":

@@ -126,6 +126,14 @@ def test_golden(path):
         cfg = pcfg() if (q.shape[1] // k.shape[1]) % 2 == 0 else pcfg(bm=128)
         out = A.prefill_varlen(q, k, v, cu, int(lens.max()), config=cfg)
         base = sdpa_prefill_bf16(q, k, v, z["cu_seqlens"], True)
+    elif str(z["kind"]) == "decode_fp8":
+        q = _t(z["q"]).to(DEV)
+        kc, vc = (torch.from_numpy(z[n]).view(torch.float8_e4m3fn).to(DEV) for n in ("k_cache", "v_cache"))
+        bt = torch.from_numpy(z["block_table"]).to(DEV)
+        sl = torch.from_numpy(z["seq_lens"]).to(DEV)
+        ks, vs = float(z["k_scale"]), float(z["v_scale"])
+        out = A.paged_decode(q, kc, vc, bt, sl, k_scale=ks, v_scale=vs)
+        base = sdpa_decode_bf16(q, (kc.float() * ks).bfloat16(), (vc.float() * vs).bfloat16(), bt, sl)
     else:
         q, kc, vc = (_t(z[n]).to(DEV) for n in ("q", "k_cache", "v_cache"))
         bt = torch.from_numpy(z["block_table"]).to(DEV)
@@ -373,6 +381,105 @@ def test_append_then_decode_equals_oracle():
     out = A.paged_decode(d.q.to(DEV), kd, vd, d.block_table.to(DEV), d.seq_lens.to(DEV))
     base = sdpa_decode_bf16(d.q.to(DEV), kd, vd, d.block_table.to(DEV), d.seq_lens.to(DEV))
     check("append+decode", out, ref, base)
+
+
+# ------------------------------------------------------------------ fp8 (e4m3) KV cache
+def run_decode_fp8(lens, Hq=32, cfg=None, seed=0, nan_tails=False):
+    shape = dict(W.C2, batch_size=len(lens), seq_len=max(lens), num_q_heads=Hq, seed=seed, kv_dtype="fp8_e4m3")
+    d = W.make_decode(shape, device="cpu", lens=lens, extra_blocks=3)
+    kc, vc = d.k_cache.clone(), d.v_cache.clone()
+    if nan_tails:  # e4m3 NaN codes (0x7f / 0xff) in every slot no sequence owns
+        bs = kc.shape[1]
+        live = torch.zeros(kc.shape[0], bs, dtype=torch.bool)
+        for b, n in enumerate(lens):
+            for t in range(n):
+                live[d.block_table[b, t // bs], t % bs] = True
+        kc.view(torch.uint8)[~live] = 0x7F
+        vc.view(torch.uint8)[~live] = 0xFF
+    ref = oracle.decode_fp8_np(d.q, kc, vc, d.block_table, d.seq_lens, d.k_scale, d.v_scale)
+    args = [t.to(DEV) for t in (d.q, kc, vc, d.block_table, d.seq_lens)]
+    out = A.paged_decode(*args, config=cfg, k_scale=d.k_scale, v_scale=d.v_scale)
+    kb = (args[1].float() * d.k_scale).bfloat16()
+    vb = (args[2].float() * d.v_scale).bfloat16()
+    if nan_tails:
+        kb, vb = torch.nan_to_num(kb), torch.nan_to_num(vb)
+    return out, ref, sdpa_decode_bf16(args[0], kb, vb, args[3], args[4])
+
+
+@pytest.mark.parametrize("hq,ns", [(8, 4), (8, 6), (16, 4), (16, 6), (32, 3), (32, 4), (32, 5), (64, 2), (64, 3)])
+def test_decode_fp8_every_variant(hq, ns):
+    out, ref, base = run_decode_fp8([1000, 333, 17, 1], Hq=hq, cfg=dcfg(0, ns, 16))
+    check(f"decode fp8 hq={hq} stages={ns}", out, ref, base)
+
+
+def test_decode_fp8_many_ragged_sequences_and_nan_tails():
+    g = torch.Generator().manual_seed(3)
+    lens = torch.randint(1, 700, (200,), generator=g).tolist()
+    lens[9] = 3000
+    out, ref, base = run_decode_fp8(lens, nan_tails=True)
+    assert not torch.isnan(out).any()
+    check("decode fp8 200 ragged seqs, NaN tails", out, ref, base)
+
+
+def test_decode_fp8_c2_full_size_subset():
+    d = W.make_decode(dict(W.C2, kv_dtype="fp8_e4m3"), device="cuda")
+    out = A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens, k_scale=d.k_scale, v_scale=d.v_scale)
+    sub = [0, 31, 63]
+    kc, vc = d.k_cache.cpu(), d.v_cache.cpu()
+    ref = oracle.decode_fp8_np(d.q[sub].cpu(), kc, vc, d.block_table[sub].cpu(), d.seq_lens[sub].cpu(),
+                               d.k_scale, d.v_scale)
+    base = sdpa_decode_bf16(d.q[sub], (d.k_cache.float() * d.k_scale).bfloat16(),
+                            (d.v_cache.float() * d.v_scale).bfloat16(), d.block_table[sub], d.seq_lens[sub])
+    check("C2 fp8 full (3 seqs checked)", out[sub], ref, base)
+
+
+def test_decode_fp8_split_config_is_invalid():
+    d = W.make_decode(dict(W.C2, batch_size=2, seq_len=64, kv_dtype="fp8_e4m3"), device="cuda")
+    with pytest.raises(A._native.B200AttnError) as e:
+        A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens, config=dcfg(0, 4, 128))
+    assert e.value.invalid
+
+
+def test_cache_append_fp8_bit_exact():
+    NB, bs, Hkv, N = 40, 16, 8, 50
+    g = torch.Generator().manual_seed(0)
+    kc = torch.zeros(NB, bs, Hkv, 128, dtype=torch.float8_e4m3fn, device=DEV)
+    vc = torch.zeros_like(kc)
+    nk = (torch.randn(N, Hkv, 128, generator=g) * 2).bfloat16()
+    nv = (torch.randn(N, Hkv, 128, generator=g) * 9).bfloat16()
+    nk[0, 0, :4] = torch.tensor([1e6, -1e6, 0.0, -0.0])  # saturation and signed zero
+    slots = torch.randperm(NB * bs, generator=g)[:N]
+    slots[3] = -1
+    ks, vs = 1 / 64, 0.05
+    A.cache_append(nk.to(DEV), nv.to(DEV), kc, vc, slots.to(DEV), k_scale=ks, v_scale=vs)
+    keep = slots >= 0
+    ek = oracle.quantize_e4m3_np(nk.float().numpy() * np.float32(1 / ks), 1.0)
+    ev = oracle.quantize_e4m3_np(nv.float().numpy() * np.float32(1 / vs), 1.0)
+    got_k = kc.view(torch.uint8).view(-1, Hkv, 128).cpu().numpy()
+    got_v = vc.view(torch.uint8).view(-1, Hkv, 128).cpu().numpy()
+    assert np.array_equal(got_k[slots[keep].numpy()], ek[keep.numpy()])
+    assert np.array_equal(got_v[slots[keep].numpy()], ev[keep.numpy()])
+    untouched = np.ones(NB * bs, dtype=bool)
+    untouched[slots[keep].numpy()] = False
+    assert not got_k[untouched].any()
+
+
+def test_append_then_decode_fp8():
+    lens = [40, 513]
+    d = W.make_decode(dict(W.C2, batch_size=2, seq_len=513, kv_dtype="fp8_e4m3"), device="cuda", lens=lens,
+                      extra_blocks=2)
+    g = torch.Generator().manual_seed(9)
+    nk, nv = ((torch.randn(2, 8, 128, generator=g)).bfloat16().to(DEV) for _ in range(2))
+    bs = 16
+    slots = torch.tensor([int(d.block_table[b, (lens[b] - 1) // bs]) * bs + (lens[b] - 1) % bs for b in range(2)],
+                         device=DEV)
+    A.cache_append(nk, nv, d.k_cache, d.v_cache, slots, k_scale=d.k_scale, v_scale=d.v_scale)
+    out = A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens, k_scale=d.k_scale, v_scale=d.v_scale)
+    ref = oracle.decode_fp8_np(d.q.cpu(), d.k_cache.cpu(), d.v_cache.cpu(), d.block_table.cpu(), d.seq_lens.cpu(),
+                               d.k_scale, d.v_scale)
+    base = sdpa_decode_bf16(d.q, (d.k_cache.float() * d.k_scale).bfloat16(), (d.v_cache.float() * d.v_scale).bfloat16(),
+                            d.block_table, d.seq_lens)
+    check("append+decode fp8", out, ref, base)
 
 
 # ------------------------------------------------------------------ runner on the GPU

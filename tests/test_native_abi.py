@@ -14,7 +14,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def header_symbols():
     text = (ROOT / "include" / "b200attn.h").read_text()
-    return set(re.findall(r"\b(b200attn_[a-z_]+)\s*\(", text))
+    return set(re.findall(r"\b(b200attn_[a-z0-9_]+)\s*\(", text))
 
 
 def test_library_exports_every_header_symbol():
@@ -23,7 +23,7 @@ def test_library_exports_every_header_symbol():
     assert syms == set(_native.EXPORTS)
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.b200attn_abi_version() == 1
+    assert lib.b200attn_abi_version() == _native.ABI_VERSION == 2
     assert lib.b200attn_status_string(2) == b"smem_overflow"
 
 
@@ -108,3 +108,32 @@ def test_product_path_refuses_cpu_tensors():
     cu = torch.tensor([0, 4], dtype=torch.int32)
     with pytest.raises(ValueError, match="CUDA"):
         A.prefill_varlen(q, q[:, :1].contiguous(), q[:, :1].contiguous(), cu, 4)
+
+
+# ------------------------------------------------------------------ fp8 (e4m3) KV-cache decode
+C2_Q, C2_CACHE = (64, 32, 128), (16384, 16, 8, 128)
+
+
+@pytest.mark.parametrize("hq,ns", [(8, 4), (8, 6), (16, 4), (16, 6), (32, 3), (32, 4), (32, 5), (64, 2), (64, 3)])
+def test_fp8_decode_compiled_variants(hq, ns):
+    rc, why = A.decode_supported((64, hq, 128), C2_CACHE, 256, 4096, dict(num_splits=0, num_stages=ns, TILE_N=16),
+                                 kv_dtype="fp8_e4m3")
+    assert rc == _native.OK, why
+
+
+def test_fp8_decode_rejections():
+    rc, why = A.decode_supported(C2_Q, C2_CACHE, 256, 4096, dict(num_splits=0, num_stages=4, TILE_N=128),
+                                 kv_dtype="fp8_e4m3")
+    assert rc == _native.UNSUPPORTED_CONFIG and "fp8" in why
+    rc, why = A.decode_supported(C2_Q, C2_CACHE, 256, 4096, dict(num_splits=0, num_stages=6, TILE_N=16),
+                                 kv_dtype="fp8_e4m3")
+    assert rc in (_native.UNSUPPORTED_CONFIG, _native.SMEM_OVERFLOW) and why
+
+
+def test_fp8_default_config_is_compiled():
+    from paper_2505_03780_b200 import dispatch
+    for hq in (8, 16, 32, 64):
+        c = dispatch.default_decode_config(batch_size=64, seq_len=4096, num_q_heads=hq, num_kv_heads=8,
+                                           head_dim=128, block_size=16, kv_dtype="fp8_e4m3")
+        rc, why = A.decode_supported((64, hq, 128), C2_CACHE, 256, 4096, c, kv_dtype="fp8_e4m3")
+        assert rc == _native.OK, (hq, c, why)

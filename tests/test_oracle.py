@@ -19,6 +19,9 @@ def test_oracle_matches_golden(path):
     z = np.load(path)
     if str(z["kind"]) == "prefill":
         out = oracle.prefill(z["q"], z["k"], z["v"], z["cu_seqlens"])
+    elif str(z["kind"]) == "decode_fp8":
+        out = oracle.decode_fp8_np(z["q"], z["k_cache"], z["v_cache"], z["block_table"], z["seq_lens"],
+                                   float(z["k_scale"]), float(z["v_scale"]))
     else:
         out = oracle.decode(z["q"], z["k_cache"], z["v_cache"], z["block_table"], z["seq_lens"])
     # golden is an fp32 kernel run; the oracle accumulates in fp64
@@ -77,3 +80,33 @@ def test_oracle_lse():
     s = np.where(np.tril(np.ones((40, 40), bool)), s, -np.inf)
     ref = np.log(np.exp(s - s.max(1, keepdims=True)).sum(1)) + s.max(1)
     assert np.abs(lse[1] - ref).max() < 1e-10
+
+
+def test_e4m3_table_matches_torch_float8():
+    """The oracle's OCP e4m3 decode table == torch.float8_e4m3fn for all 256 codes (NaN at 0x7f/0xff)."""
+    t = oracle.e4m3_table()
+    ref = torch.arange(256, dtype=torch.uint8).view(torch.float8_e4m3fn).double().numpy()
+    assert np.array_equal(np.isnan(t), np.isnan(ref))
+    ok = ~np.isnan(t)
+    assert np.array_equal(t[ok], ref[ok])
+
+
+def test_e4m3_quantizer_matches_torch_in_range():
+    x = np.random.RandomState(0).randn(200000).astype(np.float32) * 3
+    ours = oracle.quantize_e4m3_np(x, 64.0)
+    ref = (torch.from_numpy(x) * 64).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    inr = np.abs(x * 64) <= 448
+    assert np.array_equal(ours[inr], ref[inr])
+    assert set(np.unique(ours[~inr] & 0x7F)) <= {0x7E}  # saturates to +-448 (satfinite)
+
+
+def test_fp8_decode_equals_bf16_decode_on_dequantised_cache():
+    """With power-of-two scales e4m3 * scale is exact in bf16: the fp8 oracle == the (pinned) bf16 one."""
+    d = W.make_decode(dict(W.C2, batch_size=3, seq_len=200, kv_dtype="fp8_e4m3"), device="cpu",
+                      lens=[200, 1, 77], extra_blocks=2)
+    a = oracle.decode_fp8_np(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens, d.k_scale, d.v_scale)
+    kb = (d.k_cache.float() * d.k_scale).bfloat16()
+    vb = (d.v_cache.float() * d.v_scale).bfloat16()
+    assert torch.equal(kb.float(), d.k_cache.float() * d.k_scale)
+    b = oracle.decode(d.q, kb, vb, d.block_table, d.seq_lens)
+    assert np.abs(a - b).max() < 1e-12
