@@ -315,7 +315,7 @@ def run_b200(args, world, rank, local):
         plan = A.PrefillPlan(x.q, x.k, x.v, x.cu_seqlens, x.max_seqlen)
         step = plan.run
         units = x.flops
-        kernels_per_step = 1
+        kernels_per_step = 1 if len(x.lens) == 1 else 2  # + the longest-first schedule kernel
         unit = "TFLOP/s"
         scale = 1e12
         config = {"workload": "C3 varlen causal prefill (Llama-3-8B): 16 seqs 128..8192 (33430 tok), 32q/8kv, d128",
@@ -467,6 +467,22 @@ def run_b200(args, world, rank, local):
             del d4, p4, g4
         except Exception as ex:  # pragma: no cover
             extra["decode_C4_shard_of_8"] = {"error": str(ex)}
+        # C2 with an fp8 (e4m3) KV cache: same tokens, half the bytes
+        try:
+            d8 = W.make_decode(dict(W.C2, seed=rank, kv_dtype="fp8_e4m3"), device=dev)
+            p8 = A.DecodePlan(d8.q, d8.k_cache, d8.v_cache, d8.block_table, d8.seq_lens, max_seq_len=d8.max_seq_len,
+                              k_scale=d8.k_scale, v_scale=d8.v_scale)
+            g8 = capture(p8.run, n=10)
+            g8.replay()
+            t8 = cuda_time(g8.replay, 10, stream) / 10
+            bf16_ms = ms / args.steps
+            extra["decode_C2_fp8_kv"] = {"GB/s": d8.total_bytes / (t8 / 1e3) / 1e9, "ms": t8,
+                                         "frac_of_measured_hbm": d8.total_bytes / (t8 / 1e3) / 1e9 / pk["hbm_gbs"],
+                                         "kv_bytes": d8.kv_bytes, "speedup_vs_bf16_kv": bf16_ms / t8,
+                                         "variant": p8.config}
+            del d8, p8, g8
+        except Exception as ex:  # pragma: no cover
+            extra["decode_C2_fp8_kv"] = {"error": str(ex)}
 
     # ------------------------------------------------------------------ CPU baseline (rank 0, N=1)
     cpu = None
