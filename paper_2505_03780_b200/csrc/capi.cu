@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <algorithm>
 #include <mutex>
 
@@ -139,7 +140,13 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   const bool single = (p->num_seqs == 1);
   cudaError_t e;
   if (!single) {
-    b200::prefill_schedule_kernel<<<1, 1024, 0, stream>>>(p->cu_seqlens, p->num_seqs, p->causal, nkeys, ws);
+    const size_t hist_bytes = (size_t)nkeys * sizeof(int32_t);
+    if (hist_bytes <= 40 * 1024)
+      b200::prefill_schedule_kernel<true><<<1, 1024, hist_bytes, stream>>>(p->cu_seqlens, p->num_seqs, p->causal,
+                                                                           nkeys, ws);
+    else
+      b200::prefill_schedule_kernel<false><<<1, 1024, 0, stream>>>(p->cu_seqlens, p->num_seqs, p->causal, nkeys,
+                                                                   ws);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "prefill schedule launch");
   }
@@ -298,6 +305,8 @@ int num_sms() {
   return n;
 }
 
+constexpr int kFlatMinTiles = 2;
+
 size_t flat_workspace_bytes(const b200attn_decode_params* p) {
   const size_t slots = (size_t)num_sms() + p->batch;
   return slots * p->num_q_heads * (128 + 2) * sizeof(float) + ((size_t)p->batch + 1) * sizeof(int32_t);
@@ -305,15 +314,28 @@ size_t flat_workspace_bytes(const b200attn_decode_params* p) {
 
 using FlatLauncher = int (*)(const b200attn_decode_params*, bool combine, cudaStream_t);
 
+// fp8 page conversion: cvt.rn.f16x2.e4m3x2 (default, ~7% faster on C2) or, with
+// B200ATTN_FP8_HWCVT=0, the exact ALU bit conversion (no NaN/Inf can come out of it)
+bool fp8_hw_cvt() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("B200ATTN_FP8_HWCVT");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int G, int NS, bool FP8>
 int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stream) {
-  using C = b200::FlatCfg<G, NS, FP8>;
-  auto kern = b200::decode_flat_kernel<G, NS, FP8>;
-  static bool attr_done = false;
-  if (!attr_done) {
+  constexpr int KVM_ALU = FP8 ? 1 : 0;
+  using C = b200::FlatCfg<G, NS, KVM_ALU>;
+  const bool hw = FP8 && fp8_hw_cvt();
+  auto kern = hw ? b200::decode_flat_kernel<G, NS, FP8 ? 2 : 0> : b200::decode_flat_kernel<G, NS, KVM_ALU>;
+  static bool attr_done[2] = {false, false};
+  if (!attr_done[hw]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode_flat)");
-    attr_done = true;
+    attr_done[hw] = true;
   }
   const int D = 128;
   CUtensorMap mq, mk, mv;
@@ -330,8 +352,12 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
     if ((rc = make_map_3d(&mk, p->k_cache, D, tokens, 8, 8ull * D * 2, D * 2ull, C::TT, 8))) return rc;
     if ((rc = make_map_3d(&mv, p->v_cache, D, tokens, 8, 8ull * D * 2, D * 2ull, C::TT, 8))) return rc;
   }
-  const int ctas = num_sms();
-  const size_t slots = (size_t)ctas + p->batch;
+  // persistent CTAs, but at least kFlatMinTiles tiles each when the (host-known upper bound of
+  // the) tile count is small: fewer partial segments to merge, same memory parallelism
+  const long long tiles_ub = (long long)p->batch * ((p->max_seq_len + C::TT - 1) / C::TT);
+  const int ctas = (int)std::max<long long>(1, std::min<long long>(num_sms(), (tiles_ub + kFlatMinTiles - 1) /
+                                                                                  kFlatMinTiles));
+  const size_t slots = (size_t)num_sms() + p->batch;
   b200::FlatDecodeArgs a;
   a.block_table = p->block_table;
   a.seq_lens = p->seq_lens;
@@ -345,9 +371,10 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
   const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / sqrtf((float)p->head_dim);
   a.scale_log2 = scale * 1.4426950408889634f;
   a.out_scale = 1.f;
-  if (FP8) {  // converted tiles hold x * 2^-8 (see e4m3x4_to_f16x4_s8)
-    a.scale_log2 *= (p->k_scale > 0.f ? p->k_scale : 1.f) * 256.f;
-    a.out_scale = (p->v_scale > 0.f ? p->v_scale : 1.f) * 256.f;
+  if (FP8) {  // ALU-converted tiles hold x * 2^-8 (see e4m3x4_to_f16x4_s8); cvt ones hold x
+    const float f = hw ? 1.f : 256.f;
+    a.scale_log2 *= (p->k_scale > 0.f ? p->k_scale : 1.f) * f;
+    a.out_scale = (p->v_scale > 0.f ? p->v_scale : 1.f) * f;
   }
   kern<<<ctas, C::NTHREADS, C::SMEM_BYTES, stream>>>(mq, mk, mv, a);
   cudaError_t e = cudaGetLastError();
@@ -367,13 +394,12 @@ struct FlatEntry {
   FlatLauncher fn;
   int smem;
 };
-#define FF(G, NS) {G, NS, false, &launch_flat<G, NS, false>, b200::FlatCfg<G, NS, false>::SMEM_BYTES}
-#define F8(G, NS) {G, NS, true, &launch_flat<G, NS, true>, b200::FlatCfg<G, NS, true>::SMEM_BYTES}
+#define FF(G, NS) {G, NS, false, &launch_flat<G, NS, false>, b200::FlatCfg<G, NS, 0>::SMEM_BYTES}
+#define F8(G, NS) {G, NS, true, &launch_flat<G, NS, true>, b200::FlatCfg<G, NS, 1>::SMEM_BYTES}
 const FlatEntry kFlat[] = {FF(1, 3), FF(1, 4), FF(1, 5), FF(1, 6), FF(2, 3), FF(2, 4), FF(2, 5), FF(2, 6),
                            FF(4, 3), FF(4, 4), FF(4, 5), FF(8, 3), FF(8, 4),
                            // fp8 e4m3 KV: num_stages = depth of the 16-KB fp8 staging ring
-                           F8(1, 4), F8(1, 6), F8(2, 4), F8(2, 6), F8(4, 3), F8(4, 4), F8(4, 5), F8(8, 2),
-                           F8(8, 3)};
+                           F8(1, 4), F8(1, 6), F8(2, 4), F8(2, 6), F8(4, 3), F8(4, 4), F8(4, 5), F8(8, 3)};
 #undef FF
 #undef F8
 

@@ -43,12 +43,20 @@ struct FlatDecodeArgs {
   float out_scale;   // 1                        (fp8: v_scale * 2^8)
 };
 
-template <int G, int NSTAGE, bool FP8 = false>
+#ifndef B200_FP8_CONV_WARPS
+#define B200_FP8_CONV_WARPS 8
+#endif
+
+template <int G, int NSTAGE, int KVM = 0>  // KVM: 0 bf16 cache, 1 fp8 (ALU bit conversion), 2 fp8 (cvt.f16x2.e4m3x2)
 struct FlatCfg {
+  static constexpr bool FP8 = KVM != 0;
   static constexpr int D = 128, HKV = 8, TT = 16, ROWS = 128;
   static constexpr int NQ = 8 * G;
   static constexpr int NP = NQ < 16 ? 16 : NQ;  // MMA N
-  static constexpr int NTHREADS = FP8 ? 320 : 192, TMA_WARP = 4, MMA_WARP = 5, CONV_WARP0 = 6;
+  // fp8 -> fp16 converter warps: 8 (the 128-register cap of 14 warps) unless the softmax needs
+  // more registers (G = 8 keeps 64 fp32 O accumulators per thread: 4 warps, 168 registers)
+  static constexpr int NCONV = FP8 ? (G >= 8 ? 4 : B200_FP8_CONV_WARPS) : 0;
+  static constexpr int NTHREADS = 192 + 32 * NCONV, TMA_WARP = 4, MMA_WARP = 5, CONV_WARP0 = 6;
   static constexpr int SLOT = ROWS * D * 2, HALF = ROWS * 128;
   static constexpr int OPS = FP8 ? 3 : NSTAGE;   // MMA operand ring (bf16 / fp16 tiles)
   static constexpr int NSTG = FP8 ? NSTAGE : 0;  // fp8 staging ring (raw pages)
@@ -75,12 +83,14 @@ __device__ __forceinline__ int flat_cta_of(int t, int ctas, int ntiles) {
   return static_cast<int>(((static_cast<long long>(t) + 1) * ctas - 1) / ntiles);
 }
 
-template <int G, int NSTAGE, bool FP8 = false>
-__global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
+template <int G, int NSTAGE, int KVM = 0>
+__global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
     decode_flat_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
                        const __grid_constant__ CUtensorMap tmap_v, const FlatDecodeArgs args) {
-  using C = FlatCfg<G, NSTAGE, FP8>;
+  using C = FlatCfg<G, NSTAGE, KVM>;
   constexpr int NQ = C::NQ, NP = C::NP, D = C::D, OPS = C::OPS;
+  constexpr bool FP8 = C::FP8;
+  static_assert(!FP8 || C::NSTG >= 3, "fp8 staging ring must be >= 3 deep (K runs one tile ahead of V)");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sKV = smem + C::OFF_KV;
@@ -131,16 +141,16 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
     mbar_init(&q_empty[0], 1);
     mbar_init(&q_empty[1], 1);
     for (int i = 0; i < OPS; ++i) {
-      mbar_init(&kv_full[i], FP8 ? 128 : 1);
+      mbar_init(&kv_full[i], FP8 ? 32 * C::NCONV : 1);
       mbar_init(&kv_empty[i], 1);
     }
     for (int i = 0; i < C::NSTG; ++i) {
       mbar_init(&stg_full[i], 1);
-      mbar_init(&stg_empty[i], 128);
+      mbar_init(&stg_empty[i], 32 * C::NCONV);
     }
     if (FP8) {
-      mbar_init(&q_conv[0], 128);
-      mbar_init(&q_conv[1], 128);
+      mbar_init(&q_conv[0], 32 * C::NCONV);
+      mbar_init(&q_conv[1], 32 * C::NCONV);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
@@ -239,8 +249,13 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
       const uint64_t v_desc = sdesc_sw128(smem_u32(sKV), C::HALF, 1024);
       const uint64_t q_desc = sdesc_sw128(smem_u32(sQ), 16, 1024);
       const uint64_t p_desc = sdesc_sw128(smem_u32(sP), 16, 1024);
+      // operand-ring positions: bf16 = TMA order K0 V0 K1 V1 ...; fp8 = MMA consumption order
+      // K0 K1 V0 K2 V1 ... V_{n-1} (the converters fill the ring in exactly this order)
+      const int n_tiles = T1 - T0;
+      auto kpos = [&](int i) { return FP8 ? (i == 0 ? 0 : 2 * i - 1) : 2 * i; };
+      auto vpos = [&](int i) { return FP8 ? min(2 * i + 2, 2 * n_tiles - 1) : 2 * i + 1; };
       auto qk = [&](int i, int qb) {
-        const int idx = 2 * i, slot = idx % OPS;
+        const int idx = kpos(i), slot = idx % OPS;
         mbar_wait(&kv_full[slot], (idx / OPS) & 1);
         tc_fence_after();
         const uint64_t kb = k_desc + ((slot * C::SLOT) >> 4), qa = q_desc + ((qb * C::QB) >> 4);
@@ -249,7 +264,7 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
         umma_commit_w(&kv_empty[slot]);
       };
       auto pv = [&](int i) {
-        const int idx = 2 * i + 1, slot = idx % OPS;
+        const int idx = vpos(i), slot = idx % OPS;
         mbar_wait(&kv_full[slot], (idx / OPS) & 1);
         mbar_wait(&p_full[i & 1], (i >> 1) & 1);
         if (i >= 2) mbar_wait(&o_empty[i & 1], ((i >> 1) - 1) & 1);
@@ -276,51 +291,65 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
     // ------------------------------------------------------------ fp8 -> fp16 converters (FP8 only)
     const int ct = threadIdx.x - 32 * C::CONV_WARP0;
     const uint32_t stg0 = smem_u32(sSTG), kv0 = smem_u32(sKV);
-    int it = 0, k = 0, b = b_first;
+    const int n_tiles = T1 - T0;
+    // staging entry sidx (TMA order: K_i = 2i, V_i = 2i+1) -> operand position opos (MMA order)
+    auto convert = [&](int sidx, int opos) {
+      const int slot = sidx % C::NSTG, oslot = opos % OPS;
+      mbar_wait(&stg_full[slot], (sidx / C::NSTG) & 1);
+      mbar_wait(&kv_empty[oslot], ((opos / OPS) & 1) ^ 1);
+      const uint32_t src = stg0 + slot * C::STG_SLOT, dst = kv0 + oslot * C::SLOT;
+      constexpr int CT = 32 * C::NCONV;
+#pragma unroll
+      for (int j = 0; j < (1024 + CT - 1) / CT; ++j) {
+        const int id = j * CT + ct, row = id >> 3, c = id & 7;  // row = head*16 + token, 16 d per chunk
+        if (1024 % CT != 0 && id >= 1024) break;
+        const uint4 w = ld_shared_v4(src + row * 128 + c * 16);
+        uint32_t f[8];
+        if constexpr (KVM == 2) {
+          e4m3x4_to_f16x4_hw(w.x, f[0], f[1]);
+          e4m3x4_to_f16x4_hw(w.y, f[2], f[3]);
+          e4m3x4_to_f16x4_hw(w.z, f[4], f[5]);
+          e4m3x4_to_f16x4_hw(w.w, f[6], f[7]);
+        } else {
+          e4m3x4_to_f16x4_s8(w.x, f[0], f[1]);
+          e4m3x4_to_f16x4_s8(w.y, f[2], f[3]);
+          e4m3x4_to_f16x4_s8(w.z, f[4], f[5]);
+          e4m3x4_to_f16x4_s8(w.w, f[6], f[7]);
+        }
+        // d [16c, 16c+16) -> 64-col half c/4, 16-B chunks 2(c%4) and 2(c%4)+1, SW128 (chunk ^ row%8)
+        const uint32_t line = dst + (c >> 2) * C::HALF + row * 128;
+        const int x0 = (2 * c) & 7, sw = row & 7;
+        if (c < 4) {  // even chunks first for c < 4, odd first for c >= 4: no bank conflicts
+          st_shared_v4(line + ((x0 ^ sw) << 4), f[0], f[1], f[2], f[3]);
+          st_shared_v4(line + (((x0 + 1) ^ sw) << 4), f[4], f[5], f[6], f[7]);
+        } else {
+          st_shared_v4(line + (((x0 + 1) ^ sw) << 4), f[4], f[5], f[6], f[7]);
+          st_shared_v4(line + ((x0 ^ sw) << 4), f[0], f[1], f[2], f[3]);
+        }
+      }
+      mbar_arrive(&stg_empty[slot]);
+      fence_proxy_async_smem();
+      mbar_arrive(&kv_full[oslot]);
+    };
+    int i = 0, k = 0, b = b_first;
     for (int t = T0; t < T1; ++k) {
       while (cu[b + 1] <= t) ++b;
       const int seg_end = min(T1, cu[b + 1]);
       mbar_wait(&q_full[k & 1], (k >> 1) & 1);
       uint32_t* qw = reinterpret_cast<uint32_t*>(sQ + (k & 1) * C::QB);
-      for (int x = ct; x < NQ * 64; x += 128) {  // rows >= NQ are zero padding (0 -> 0)
+      for (int x = ct; x < NQ * 64; x += 32 * C::NCONV) {  // rows >= NQ are zero padding (0 -> 0)
         const int r = x >> 6, h = (x >> 5) & 1, w = x & 31;  // row, 64-col half, word in the 128-B line
         qw[h * (C::QHALF / 4) + r * 32 + w] = bf16x2_to_f16x2(qw[h * (C::QHALF / 4) + r * 32 + w]);
       }
       fence_proxy_async_smem();
       mbar_arrive(&q_conv[k & 1]);
-      for (; t < seg_end; ++t) {
 #pragma unroll 1
-        for (int kv = 0; kv < 2; ++kv, ++it) {
-          const int slot = it % C::NSTG, oslot = it % OPS;
-          mbar_wait(&stg_full[slot], (it / C::NSTG) & 1);
-          mbar_wait(&kv_empty[oslot], ((it / OPS) & 1) ^ 1);
-          const uint32_t src = stg0 + slot * C::STG_SLOT, dst = kv0 + oslot * C::SLOT;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int id = j * 128 + ct, row = id >> 3, c = id & 7;  // row = head*16 + token, 16 d per chunk
-            const uint4 w = ld_shared_v4(src + row * 128 + c * 16);
-            uint32_t f[8];
-            e4m3x4_to_f16x4_s8(w.x, f[0], f[1]);
-            e4m3x4_to_f16x4_s8(w.y, f[2], f[3]);
-            e4m3x4_to_f16x4_s8(w.z, f[4], f[5]);
-            e4m3x4_to_f16x4_s8(w.w, f[6], f[7]);
-            // d [16c, 16c+16) -> 64-col half c/4, 16-B chunks 2(c%4) and 2(c%4)+1, SW128 (chunk ^ row%8)
-            const uint32_t line = dst + (c >> 2) * C::HALF + row * 128;
-            const int x0 = (2 * c) & 7, sw = row & 7;
-            if (c < 4) {  // even chunks first for c < 4, odd first for c >= 4: no bank conflicts
-              st_shared_v4(line + ((x0 ^ sw) << 4), f[0], f[1], f[2], f[3]);
-              st_shared_v4(line + (((x0 + 1) ^ sw) << 4), f[4], f[5], f[6], f[7]);
-            } else {
-              st_shared_v4(line + (((x0 + 1) ^ sw) << 4), f[4], f[5], f[6], f[7]);
-              st_shared_v4(line + ((x0 ^ sw) << 4), f[0], f[1], f[2], f[3]);
-            }
-          }
-          mbar_arrive(&stg_empty[slot]);
-          fence_proxy_async_smem();
-          mbar_arrive(&kv_full[oslot]);
-        }
+      for (; t < seg_end; ++t, ++i) {
+        convert(2 * i, i == 0 ? 0 : 2 * i - 1);                          // K_i
+        if (i >= 1) convert(2 * i - 1, min(2 * i, 2 * n_tiles - 1));   // V_{i-1}
       }
     }
+    convert(2 * n_tiles - 1, 2 * n_tiles - 1);  // V_{n-1}
   } else {
     // ------------------------------------------------------------ softmax / fold / epilogue
     const int row = threadIdx.x;  // S^T row (head*16 + token) and O^T row (d)
@@ -396,11 +425,11 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
                        : "memory");
           if (t16 == 0) alpha_s[(i % 3) * NP + qh] = alpha[g];
         }
-        if (!FP8 && !valid) {
+        if (KVM != 1 && !valid) {
           // the page's tail slots past the sequence end hold arbitrary bytes: P = 0 there, but
-          // 0 * NaN would poison O, so zero this row of the V tile before PV reads it (the fp8
-          // conversion cannot produce NaN/Inf, so the FP8 path needs no zeroing)
-          const int vidx = 2 * i + 1, vslot = vidx % OPS;
+          // 0 * NaN would poison O, so zero this row of the V tile before PV reads it (the ALU
+          // fp8 conversion, KVM 1, cannot produce NaN/Inf and needs no zeroing)
+          const int vidx = FP8 ? min(2 * i + 2, 2 * (T1 - T0) - 1) : 2 * i + 1, vslot = vidx % OPS;
           mbar_wait(&kv_full[vslot], (vidx / OPS) & 1);
           uint4* vr = reinterpret_cast<uint4*>(sKV + vslot * C::SLOT + row * 128);
 #pragma unroll
@@ -458,37 +487,105 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
 }
 
 // K3': merge the partial segments of every split sequence (sequences finished inside one CTA
-// were already written by it).
+// were already written by it).  One CTA per (sequence, q head); the up-to-148 partials of a
+// sequence are reduced in parallel — max and weights across threads, then each warp sums a
+// quarter of the partial rows with float4 loads (4 in flight per lane) — instead of one
+// dependent load chain per partial (which made a 1-sequence decode latency-bound at ~100 us).
+constexpr int kFlatMaxCtas = 1024;
+
 template <int NQ>
 __global__ void __launch_bounds__(128) flat_combine_kernel(const float* __restrict__ part_o,
                                                            const float* __restrict__ part_ml,
                                                            const int32_t* __restrict__ cu, int batch, int ctas,
                                                            __nv_bfloat16* __restrict__ o) {
-  const int b = blockIdx.x, q = blockIdx.y, d = threadIdx.x;
+  __shared__ float sw[kFlatMaxCtas];
+  __shared__ float red[4];
+  __shared__ float4 acc_s[4][32];
+  const int b = blockIdx.x, q = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ts = cu[b], te = cu[b + 1], n = cu[batch];
-  __nv_bfloat16* out = o + (static_cast<size_t>(b) * NQ + q) * 128 + d;
+  __nv_bfloat16* out = o + (static_cast<size_t>(b) * NQ + q) * 128;
   if (ts == te) {
-    *out = __float2bfloat16_rn(0.f);
+    out[tid] = __float2bfloat16_rn(0.f);
     return;
   }
   const int c0 = flat_cta_of(ts, ctas, n), c1 = flat_cta_of(te - 1, ctas, n);
   if (c0 == c1) return;
+  const int nc = c1 - c0 + 1;
   // CTAs whose range is empty (fewer tiles than CTAs) wrote nothing: skip their slots
   auto owns = [&](int c) {
     return static_cast<long long>(c) * n / ctas != (static_cast<long long>(c) + 1) * n / ctas;
   };
-  float M = -INFINITY;
-  for (int c = c0; c <= c1; ++c)
-    if (owns(c)) M = fmaxf(M, part_ml[((static_cast<size_t>(c) + b) * NQ + q) * 2]);
-  float acc = 0.f, L = 0.f;
-  for (int c = c0; c <= c1; ++c) {
-    if (!owns(c)) continue;
-    const size_t slot = static_cast<size_t>(c) + b;
-    const float w = fast_exp2(part_ml[(slot * NQ + q) * 2] - M);
-    L = fmaf(w, part_ml[(slot * NQ + q) * 2 + 1], L);
-    acc = fmaf(w, part_o[(slot * NQ + q) * 128 + d], acc);
+  auto ml = [&](int c, int k) { return part_ml[((static_cast<size_t>(c) + b) * NQ + q) * 2 + k]; };
+  float m = -INFINITY;
+  for (int i = tid; i < nc; i += 128)
+    if (owns(c0 + i)) m = fmaxf(m, ml(c0 + i, 0));
+#pragma unroll
+  for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  const float M = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  __syncthreads();
+  float l = 0.f;
+  for (int i = tid; i < nc; i += 128) {
+    const int c = c0 + i;
+    const float w = owns(c) ? fast_exp2(ml(c, 0) - M) : 0.f;
+    sw[i] = w;
+    if (w != 0.f) l = fmaf(w, ml(c, 1), l);
   }
-  *out = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+  if (lane == 0) red[warp] = l;
+  __syncthreads();
+  const float L = red[0] + red[1] + red[2] + red[3];
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto row = [&](int i) {
+    return reinterpret_cast<const float4*>(part_o + ((static_cast<size_t>(c0 + i) + b) * NQ + q) * 128) + lane;
+  };
+  int i = warp;
+  for (; i + 12 < nc; i += 16) {  // 4 partial rows per warp per round, loads issued back to back
+    float4 v[4];
+    float w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      w[u] = sw[i + 4 * u];
+      v[u] = w[u] != 0.f ? __ldg(row(i + 4 * u)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc.x = fmaf(w[u], v[u].x, acc.x);
+      acc.y = fmaf(w[u], v[u].y, acc.y);
+      acc.z = fmaf(w[u], v[u].z, acc.z);
+      acc.w = fmaf(w[u], v[u].w, acc.w);
+    }
+  }
+  for (; i < nc; i += 4) {
+    const float w = sw[i];
+    if (w != 0.f) {
+      const float4 v = __ldg(row(i));
+      acc.x = fmaf(w, v.x, acc.x);
+      acc.y = fmaf(w, v.y, acc.y);
+      acc.z = fmaf(w, v.z, acc.z);
+      acc.w = fmaf(w, v.w, acc.w);
+    }
+  }
+  acc_s[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    float4 r = acc_s[0][lane];
+#pragma unroll
+    for (int k = 1; k < 4; ++k) {
+      r.x += acc_s[k][lane].x;
+      r.y += acc_s[k][lane].y;
+      r.z += acc_s[k][lane].z;
+      r.w += acc_s[k][lane].w;
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(r.x * inv, r.y * inv), hi = __floats2bfloat162_rn(r.z * inv, r.w * inv);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(out + 4 * lane) = pk;
+  }
 }
 
 }  // namespace b200

@@ -447,6 +447,14 @@ __device__ __forceinline__ void e4m3x4_to_f16x4_s8(uint32_t w, uint32_t& lo, uin
   hi = (b << 7) & 0xBF80BF80u;
 }
 
+// Same with the hardware converter (exact, unscaled): two cvt.rn.f16x2.e4m3x2.
+__device__ __forceinline__ void e4m3x4_to_f16x4_hw(uint32_t w, uint32_t& lo, uint32_t& hi) {
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+      "cvt.rn.f16x2.e4m3x2 %0, l;\n\tcvt.rn.f16x2.e4m3x2 %1, h;\n\t}"
+      : "=r"(lo), "=r"(hi)
+      : "r"(w));
+}
+
 // bf16 pair -> fp16 pair (round to nearest); used to retype Q for the fp16 MMA of the fp8 path.
 __device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t w) {
   uint32_t r;

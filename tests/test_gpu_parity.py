@@ -406,7 +406,7 @@ def run_decode_fp8(lens, Hq=32, cfg=None, seed=0, nan_tails=False):
     return out, ref, sdpa_decode_bf16(args[0], kb, vb, args[3], args[4])
 
 
-@pytest.mark.parametrize("hq,ns", [(8, 4), (8, 6), (16, 4), (16, 6), (32, 3), (32, 4), (32, 5), (64, 2), (64, 3)])
+@pytest.mark.parametrize("hq,ns", [(8, 4), (8, 6), (16, 4), (16, 6), (32, 3), (32, 4), (32, 5), (64, 3)])
 def test_decode_fp8_every_variant(hq, ns):
     out, ref, base = run_decode_fp8([1000, 333, 17, 1], Hq=hq, cfg=dcfg(0, ns, 16))
     check(f"decode fp8 hq={hq} stages={ns}", out, ref, base)
