@@ -60,6 +60,7 @@ struct FlatCfg {
   static constexpr int SLOT = ROWS * D * 2, HALF = ROWS * 128;
   static constexpr int OPS = FP8 ? 3 : NSTAGE;   // MMA operand ring (bf16 / fp16 tiles)
   static constexpr int NSTG = FP8 ? NSTAGE : 0;  // fp8 staging ring (raw pages)
+  static constexpr int NSTG_DIV = NSTG > 0 ? NSTG : 1;  // divisor for ring arithmetic (bf16: dead code)
   static constexpr int STG_SLOT = ROWS * D;      // one fp8 page of 8 kv heads x 16 tokens
   static constexpr int QB = NP * 256, QHALF = NP * 128;
   static constexpr int PB = NP * 256, PHALF = NP * 128;
@@ -68,15 +69,15 @@ struct FlatCfg {
   static constexpr int OFF_STG = OFF_KV + OPS * SLOT;
   static constexpr int OFF_Q = OFF_STG + NSTG * STG_SLOT;
   static constexpr int OFF_P = OFF_Q + 2 * QB;
-  static constexpr int OFF_ALPHA = OFF_P + 2 * PB;     // [3][NP] f32
+  static constexpr int OFF_ALPHA = OFF_P + 2 * PB;     // [NP] f32 rescale factors + int32 flags[2][4]
   static constexpr int OFF_ML = OFF_ALPHA + 3 * NP * 4;  // [2][NP] f32
   static constexpr int OFF_CU = OFF_ML + 2 * NP * 4;     // [MAXB + 1] i32
   static constexpr int OFF_BAR = (OFF_CU + (MAXB + 1) * 4 + 7) & ~7;
   static constexpr int NUM_BARS = 4 + 2 * OPS + 8 + 2 * NSTG + 2;
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
   static constexpr uint32_t TMEM_COLS = (4 * NP <= 64) ? 64 : (4 * NP <= 128 ? 128 : 256);
-  __host__ __device__ static constexpr uint32_t S_COL(int i) { return (i & 1) * NP; }
-  __host__ __device__ static constexpr uint32_t O_COL(int i) { return 2 * NP + (i & 1) * NP; }
+  __host__ __device__ static constexpr uint32_t S_COL(int i) { return (i & 1) * NP; }  // per tile
+  __host__ __device__ static constexpr uint32_t O_COL(int k) { return 2 * NP + (k & 1) * NP; }  // per segment
 };
 
 __device__ __forceinline__ int flat_cta_of(int t, int ctas, int ntiles) {
@@ -218,8 +219,8 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
           if (FP8 && lane == 0) {
 #pragma unroll
             for (int kv = 0; kv < 2; ++kv, ++it) {
-              const int slot = it % C::NSTG;
-              mbar_wait(&stg_empty[slot], ((it / C::NSTG) & 1) ^ 1);
+              const int slot = it % C::NSTG_DIV;
+              mbar_wait(&stg_empty[slot], ((it / C::NSTG_DIV) & 1) ^ 1);
               mbar_arrive_expect_tx(&stg_full[slot], C::STG_SLOT);
               tma_load_3d_hint(sSTG + slot * C::STG_SLOT, kv ? &tmap_v : &tmap_k, &stg_full[slot], 0, row, 0,
                                stream_once);
@@ -263,29 +264,34 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
         umma_commit_w(&s_full[i & 1]);
         umma_commit_w(&kv_empty[slot]);
       };
-      auto pv = [&](int i) {
+      // PV of tile i accumulates into segment seg's O buffer (fresh on the segment's first tile,
+      // which first waits for the epilogue of segment seg-2 to release the buffer)
+      auto pv = [&](int i, int seg, bool first) {
         const int idx = vpos(i), slot = idx % OPS;
         mbar_wait(&kv_full[slot], (idx / OPS) & 1);
         mbar_wait(&p_full[i & 1], (i >> 1) & 1);
-        if (i >= 2) mbar_wait(&o_empty[i & 1], ((i >> 1) - 1) & 1);
+        if (first && seg >= 2) mbar_wait(&o_empty[seg & 1], ((seg >> 1) - 1) & 1);
         tc_fence_after();
         const uint64_t vb = v_desc + ((slot * C::SLOT) >> 4), pb = p_desc + (((i & 1) * C::PB) >> 4);
-        umma_ss_k128<128, 512, 2, C::PHALF / 16>(tmem + C::O_COL(i), vb, pb, IDESC_PV, 0u);
-        umma_commit_w(&o_full[i & 1]);
+        umma_ss_k128<128, 512, 2, C::PHALF / 16>(tmem + C::O_COL(seg), vb, pb, IDESC_PV, first ? 0u : 1u);
+        umma_commit_w(&o_full[i & 1]);  // PV(i) lands: o_full[i & 1], phase (i >> 1) & 1
         umma_commit_w(&kv_empty[slot]);
       };
-      int i = 0, k = 0, b = b_first;
+      int i = 0, k = 0, b = b_first, pk = 0;
+      bool pfirst = false;
       for (int t = T0; t < T1; ++k) {
         while (cu[b + 1] <= t) ++b;
-        const int seg_end = min(T1, cu[b + 1]);
+        const int seg_end = min(T1, cu[b + 1]), seg_t0 = t;
         mbar_wait(FP8 ? &q_conv[k & 1] : &q_full[k & 1], (k >> 1) & 1);
         for (; t < seg_end; ++t, ++i) {
           qk(i, k & 1);
           if (t == seg_end - 1) umma_commit_w(&q_empty[k & 1]);
-          if (i >= 1) pv(i - 1);
+          if (i >= 1) pv(i - 1, pk, pfirst);
+          pk = k;
+          pfirst = (t == seg_t0);
         }
       }
-      pv(i - 1);
+      pv(i - 1, pk, pfirst);
     }
   } else if (FP8 && warp >= C::CONV_WARP0) {
     // ------------------------------------------------------------ fp8 -> fp16 converters (FP8 only)
@@ -294,11 +300,11 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
     const int n_tiles = T1 - T0;
     // staging entry sidx (TMA order: K_i = 2i, V_i = 2i+1) -> operand position opos (MMA order)
     auto convert = [&](int sidx, int opos) {
-      const int slot = sidx % C::NSTG, oslot = opos % OPS;
-      mbar_wait(&stg_full[slot], (sidx / C::NSTG) & 1);
+      const int slot = sidx % C::NSTG_DIV, oslot = opos % OPS;
+      mbar_wait(&stg_full[slot], (sidx / C::NSTG_DIV) & 1);
       mbar_wait(&kv_empty[oslot], ((opos / OPS) & 1) ^ 1);
       const uint32_t src = stg0 + slot * C::STG_SLOT, dst = kv0 + oslot * C::SLOT;
-      constexpr int CT = 32 * C::NCONV;
+      constexpr int CT = C::NCONV > 0 ? 32 * C::NCONV : 32;
 #pragma unroll
       for (int j = 0; j < (1024 + CT - 1) / CT; ++j) {
         const int id = j * CT + ct, row = id >> 3, c = id & 7;  // row = head*16 + token, 16 d per chunk
@@ -351,7 +357,12 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
     }
     convert(2 * n_tiles - 1, 2 * n_tiles - 1);  // V_{n-1}
   } else {
-    // ------------------------------------------------------------ softmax / fold / epilogue
+    // ------------------------------------------------------------ softmax + epilogue
+    // O^T accumulates in TMEM across a segment's tiles (PV with acc = 1).  Exponentials use the
+    // running max m_run, which only moves when a score exceeds it by more than 8 (log2 units,
+    // FA4's lazy rescale): then, and on a segment's first tile, the CTA takes the slow path —
+    // exact per-head max (16-lane shuffles), alpha to smem, and once PV(i-1) has landed every
+    // thread rescales its O^T row in TMEM.  The common tile is a vote, G exp2 and G P stores.
     const int row = threadIdx.x;  // S^T row (head*16 + token) and O^T row (d)
     const int h = row >> 4, t16 = row & 15;
     const bool upper = (lane >> 4) != 0;
@@ -360,22 +371,11 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
     const float sl2 = args.scale_log2;
     const uint32_t p_base = smem_u32(sP) + (row >> 6) * C::PHALF + (row & 7) * 2;
     const int rchunk = (row & 63) >> 3;
+    volatile int* flags = reinterpret_cast<volatile int*>(alpha_s + NP);  // [2][4] per-warp votes
 
-    float m_run[G], l_part[G], o_acc[NQ];
-    auto fold = [&](int j) {
-      mbar_wait(&o_full[j & 1], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t r[NQ];
-      tmem_ld_cols<NQ>(tmem + lane_base + C::O_COL(j), r);
-      const float* al = alpha_s + (j % 3) * NP;
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) o_acc[q] = fmaf(o_acc[q], al[q], __uint_as_float(r[q]));
-      tc_fence_before();
-      mbar_arrive(&o_empty[j & 1]);
-    };
-
+    float m_run[G], l_part[G];
     int i = 0, b = b_first;
-    for (int t = T0; t < T1;) {
+    for (int t = T0, k = 0; t < T1; ++k) {
       while (cu[b + 1] <= t) ++b;
       const int seg_end = min(T1, cu[b + 1]);
       const int tile0 = cu[b];
@@ -386,9 +386,7 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
         m_run[g] = -INFINITY;
         l_part[g] = 0.f;
       }
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) o_acc[q] = 0.f;
-      const int first_i = i;
+      const int seg_i0 = i;
       for (; t < seg_end; ++t, ++i) {
         const int sb = i & 1;
         mbar_wait(&s_full[sb], (i >> 1) & 1);
@@ -397,21 +395,49 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
         tmem_ld_cols<2 * G>(tmem + lane_base + C::S_COL(i) + col_base, sv);
         const int tok = (t - tile0) * C::TT + t16;
         const bool valid = tok < len;
-        float alpha[G];
+        float x[G];
+        bool need = false;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          x[g] = valid ? __uint_as_float(upper ? sv[G + g] : sv[g]) * sl2 : -INFINITY;
+          need |= x[g] > m_run[g] + 8.0f;
+        }
+        const bool warp_need = __any_sync(0xffffffffu, need);
+        if (lane == 0) flags[sb * 4 + warp] = warp_need;
+        named_bar_sync(1, 128);
+        if (flags[sb * 4 + 0] | flags[sb * 4 + 1] | flags[sb * 4 + 2] | flags[sb * 4 + 3]) {
+          // slow path (CTA-uniform): exact head maxima, rescale factors, O rescale
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            float mt = x[g];
+#pragma unroll
+            for (int off = 1; off < 16; off <<= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
+            float alpha = 1.f;
+            if (mt > m_run[g] + 8.0f) {
+              alpha = (m_run[g] == -INFINITY) ? 0.f : fast_exp2(m_run[g] - mt);
+              m_run[g] = mt;
+              l_part[g] *= alpha;
+            }
+            if (t16 == 0) alpha_s[h * G + g] = alpha;
+          }
+          named_bar_sync(1, 128);
+          if (i > seg_i0) {  // O holds tiles seg_i0 .. i-1: rescale once PV(i-1) has landed
+            mbar_wait(&o_full[(i - 1) & 1], ((i - 1) >> 1) & 1);
+            tc_fence_after();
+            uint32_t r[NQ];
+            tmem_ld_cols<NQ>(tmem + lane_base + C::O_COL(k), r);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) * alpha_s[q]);
+            tmem_st_cols<NQ>(tmem + lane_base + C::O_COL(k), r);
+            tmem_wait_st();
+          }
+        }
         const uint32_t pb = p_base + sb * C::PB;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          const float s = __uint_as_float(upper ? sv[G + g] : sv[g]);
-          const float x = valid ? s * sl2 : -INFINITY;
-          float mt = x;
-#pragma unroll
-          for (int off = 1; off < 16; off <<= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
-          const float mn = fmaxf(m_run[g], mt);
-          const float mu = (mn == -INFINITY) ? 0.f : mn;
-          alpha[g] = fast_exp2(m_run[g] - mu);
-          const float p = fast_exp2(x - mu);
-          l_part[g] = fmaf(l_part[g], alpha[g], p);
-          m_run[g] = mn;
+          const float mu = (m_run[g] == -INFINITY) ? 0.f : m_run[g];
+          const float p = fast_exp2(x[g] - mu);  // x = -inf (invalid / masked) -> 0
+          l_part[g] += p;
           const int qh = h * G + g;
           uint16_t pbits;
           if constexpr (FP8) {
@@ -423,7 +449,6 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
           }
           asm volatile("st.shared.b16 [%0], %1;" ::"r"(pb + qh * 128 + ((rchunk ^ (qh & 7)) << 4)), "h"(pbits)
                        : "memory");
-          if (t16 == 0) alpha_s[(i % 3) * NP + qh] = alpha[g];
         }
         if (KVM != 1 && !valid) {
           // the page's tail slots past the sequence end hold arbitrary bytes: P = 0 there, but
@@ -441,12 +466,9 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
-        named_bar_sync(1, 128);  // alpha_s[i % 3] visible to every fold
-        if (i > first_i) fold(i - 1);
       }
-      fold(i - 1);
 
-      // ---- segment epilogue
+      // ---- segment epilogue: O^T (TMEM) / l, or the unnormalised partial for K3'
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         float l = l_part[g];
@@ -457,23 +479,32 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
           ml_s[NP + h * G + g] = l;
         }
       }
-      named_bar_sync(1, 128);
+      // last PV of this segment (in-order completion: every earlier PV has landed too).  Per-parity
+      // barriers keep the phase unambiguous: PV(i-3) is complete and PV(i+1) cannot be issued yet.
+      mbar_wait(&o_full[(i - 1) & 1], ((i - 1) >> 1) & 1);
+      tc_fence_after();
+      uint32_t r[NQ];
+      tmem_ld_cols<NQ>(tmem + lane_base + C::O_COL(k), r);
+      tc_fence_before();
+      mbar_arrive(&o_empty[k & 1]);
+      named_bar_sync(1, 128);  // ml_s visible
       if (complete) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
           const float l = ml_s[NP + q];
           args.o[(static_cast<size_t>(b) * NQ + q) * D + row] =
-              __float2bfloat16_rn(l > 0.f ? o_acc[q] * args.out_scale / l : 0.f);
+              __float2bfloat16_rn(l > 0.f ? __uint_as_float(r[q]) * args.out_scale / l : 0.f);
         }
       } else {
         const size_t slot = static_cast<size_t>(blockIdx.x) + b;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) args.part_o[(slot * NQ + q) * D + row] = o_acc[q] * args.out_scale;
+        for (int q = 0; q < NQ; ++q) args.part_o[(slot * NQ + q) * D + row] = __uint_as_float(r[q]) * args.out_scale;
         if (row < NQ) {
           args.part_ml[(slot * NQ + row) * 2 + 0] = ml_s[row];
           args.part_ml[(slot * NQ + row) * 2 + 1] = ml_s[NP + row];
         }
       }
+      named_bar_sync(1, 128);  // ml_s reads done before the next segment's epilogue rewrites it
     }
   }
 
