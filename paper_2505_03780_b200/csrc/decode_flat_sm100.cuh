@@ -142,16 +142,16 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
     mbar_init(&q_empty[0], 1);
     mbar_init(&q_empty[1], 1);
     for (int i = 0; i < OPS; ++i) {
-      mbar_init(&kv_full[i], FP8 ? 32 * C::NCONV : 1);
+      mbar_init(&kv_full[i], FP8 ? C::NCONV : 1);
       mbar_init(&kv_empty[i], 1);
     }
     for (int i = 0; i < C::NSTG; ++i) {
       mbar_init(&stg_full[i], 1);
-      mbar_init(&stg_empty[i], 32 * C::NCONV);
+      mbar_init(&stg_empty[i], C::NCONV);
     }
     if (FP8) {
-      mbar_init(&q_conv[0], 32 * C::NCONV);
-      mbar_init(&q_conv[1], 32 * C::NCONV);
+      mbar_init(&q_conv[0], C::NCONV);
+      mbar_init(&q_conv[1], C::NCONV);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
@@ -299,17 +299,23 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
     const uint32_t stg0 = smem_u32(sSTG), kv0 = smem_u32(sKV);
     const int n_tiles = T1 - T0;
     // staging entry sidx (TMA order: K_i = 2i, V_i = 2i+1) -> operand position opos (MMA order)
+    // thread ct converts the 16-byte chunk c = ct % 8 of rows r0 + j*CT/8 (row = head*16 + token,
+    // 16 d per chunk); CT/8 is a multiple of 8, so the swizzle phase row % 8 is per-thread constant
+    constexpr int CT = C::NCONV > 0 ? 32 * C::NCONV : 32;
+    static_assert(!FP8 || (1024 % CT == 0 && (CT / 8) % 8 == 0), "converter thread mapping");
+    const int c = ct & 7, r0 = ct >> 3, sw = r0 & 7, x0 = (2 * c) & 7;
+    const uint32_t src_off = r0 * 128 + c * 16;
+    const uint32_t line_off = (c >> 2) * C::HALF + r0 * 128;
+    const uint32_t d_lo = line_off + ((x0 ^ sw) << 4), d_hi = line_off + (((x0 + 1) ^ sw) << 4);
     auto convert = [&](int sidx, int opos) {
       const int slot = sidx % C::NSTG_DIV, oslot = opos % OPS;
       mbar_wait(&stg_full[slot], (sidx / C::NSTG_DIV) & 1);
       mbar_wait(&kv_empty[oslot], ((opos / OPS) & 1) ^ 1);
-      const uint32_t src = stg0 + slot * C::STG_SLOT, dst = kv0 + oslot * C::SLOT;
-      constexpr int CT = C::NCONV > 0 ? 32 * C::NCONV : 32;
+      const uint32_t src = stg0 + slot * C::STG_SLOT + src_off, dst = kv0 + oslot * C::SLOT;
 #pragma unroll
-      for (int j = 0; j < (1024 + CT - 1) / CT; ++j) {
-        const int id = j * CT + ct, row = id >> 3, c = id & 7;  // row = head*16 + token, 16 d per chunk
-        if (1024 % CT != 0 && id >= 1024) break;
-        const uint4 w = ld_shared_v4(src + row * 128 + c * 16);
+      for (int j = 0; j < 1024 / CT; ++j) {
+        const uint32_t rstep = j * (CT / 8) * 128;
+        const uint4 w = ld_shared_v4(src + rstep);
         uint32_t f[8];
         if constexpr (KVM == 2) {
           e4m3x4_to_f16x4_hw(w.x, f[0], f[1]);
@@ -323,19 +329,21 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
           e4m3x4_to_f16x4_s8(w.w, f[6], f[7]);
         }
         // d [16c, 16c+16) -> 64-col half c/4, 16-B chunks 2(c%4) and 2(c%4)+1, SW128 (chunk ^ row%8)
-        const uint32_t line = dst + (c >> 2) * C::HALF + row * 128;
-        const int x0 = (2 * c) & 7, sw = row & 7;
+        const uint32_t line = dst + rstep;
         if (c < 4) {  // even chunks first for c < 4, odd first for c >= 4: no bank conflicts
-          st_shared_v4(line + ((x0 ^ sw) << 4), f[0], f[1], f[2], f[3]);
-          st_shared_v4(line + (((x0 + 1) ^ sw) << 4), f[4], f[5], f[6], f[7]);
+          st_shared_v4(line + d_lo, f[0], f[1], f[2], f[3]);
+          st_shared_v4(line + d_hi, f[4], f[5], f[6], f[7]);
         } else {
-          st_shared_v4(line + (((x0 + 1) ^ sw) << 4), f[4], f[5], f[6], f[7]);
-          st_shared_v4(line + ((x0 ^ sw) << 4), f[0], f[1], f[2], f[3]);
+          st_shared_v4(line + d_hi, f[4], f[5], f[6], f[7]);
+          st_shared_v4(line + d_lo, f[0], f[1], f[2], f[3]);
         }
       }
-      mbar_arrive(&stg_empty[slot]);
-      fence_proxy_async_smem();
-      mbar_arrive(&kv_full[oslot]);
+      fence_proxy_async_smem();  // this thread's operand writes -> async proxy
+      __syncwarp();
+      if (lane == 0) {  // one arrival per converter warp
+        mbar_arrive(&stg_empty[slot]);
+        mbar_arrive(&kv_full[oslot]);
+      }
     };
     int i = 0, k = 0, b = b_first;
     for (int t = T0; t < T1; ++k) {
@@ -348,7 +356,8 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
         qw[h * (C::QHALF / 4) + r * 32 + w] = bf16x2_to_f16x2(qw[h * (C::QHALF / 4) + r * 32 + w]);
       }
       fence_proxy_async_smem();
-      mbar_arrive(&q_conv[k & 1]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&q_conv[k & 1]);
 #pragma unroll 1
       for (; t < seg_end; ++t, ++i) {
         convert(2 * i, i == 0 ? 0 : 2 * i - 1);                          // K_i
