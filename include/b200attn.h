@@ -155,7 +155,9 @@ int b200attn_cache_append_fp8(const void* new_k, const void* new_v, void* k_cach
  *   mode 1: D[128x128]  = A[128x128] . B[128x128]     B MN-major ([K][N] row-major)
  *   mode 2: D[128x16]   = A^T . B^T   with A [128(K)][128(M)] MN-major, B [16][128] K-major
  *   mode 3: D[128x128]  = A . B^T     with A staged in TMEM (bf16x2 per column), B K-major (TS MMA)
- * A, B bf16 device pointers; D fp32 device pointer. */
+ *   mode 4: D[128x128]  = A . B^T     e4m3 bytes (kind::f8f6f4), A [M][K] and B [N][K] K-major
+ *   mode 5: D[128x128]  = A . B^T     e4m3 bytes, A given as [K][M] (MN-major), B K-major
+ * A, B bf16 (modes 0-3) or e4m3 byte (modes 4-5) device pointers; D fp32 device pointer. */
 int b200attn_selftest_umma(int mode, const void* a, const void* b, float* d, void* stream);
 
 #ifdef __cplusplus

@@ -80,7 +80,7 @@ int make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint
   return B200ATTN_OK;
 }
 
-// 3-D byte map (fp8 pages) over [d2][d1][d0] with a {box0, box1, box2} unswizzled box.
+// 3-D byte map (fp8 pages) over [d2][d1][d0] with a {box0 = 128, box1, box2} SWIZZLE_128B box.
 int make_map_u8_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
                    uint64_t stride2_bytes, uint32_t box0, uint32_t box1, uint32_t box2) {
   auto fn = encode_fn();
@@ -90,7 +90,7 @@ int make_map_u8_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, u
   cuuint32_t box[3] = {box0, box1, box2};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(B200ATTN_BAD_ARGS, "cuTensorMapEncodeTiled(u8) failed (%d)", static_cast<int>(r));
@@ -314,28 +314,15 @@ size_t flat_workspace_bytes(const b200attn_decode_params* p) {
 
 using FlatLauncher = int (*)(const b200attn_decode_params*, bool combine, cudaStream_t);
 
-// fp8 page conversion: cvt.rn.f16x2.e4m3x2 (default, ~7% faster on C2) or, with
-// B200ATTN_FP8_HWCVT=0, the exact ALU bit conversion (no NaN/Inf can come out of it)
-bool fp8_hw_cvt() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("B200ATTN_FP8_HWCVT");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 template <int G, int NS, bool FP8>
 int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stream) {
-  constexpr int KVM_ALU = FP8 ? 1 : 0;
-  using C = b200::FlatCfg<G, NS, KVM_ALU>;
-  const bool hw = FP8 && fp8_hw_cvt();
-  auto kern = hw ? b200::decode_flat_kernel<G, NS, FP8 ? 2 : 0> : b200::decode_flat_kernel<G, NS, KVM_ALU>;
-  static bool attr_done[2] = {false, false};
-  if (!attr_done[hw]) {
+  using C = b200::FlatCfg<G, NS, FP8>;
+  auto kern = b200::decode_flat_kernel<G, NS, FP8>;
+  static bool attr_done = false;
+  if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode_flat)");
-    attr_done[hw] = true;
+    attr_done = true;
   }
   const int D = 128;
   CUtensorMap mq, mk, mv;
@@ -371,10 +358,9 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
   const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / sqrtf((float)p->head_dim);
   a.scale_log2 = scale * 1.4426950408889634f;
   a.out_scale = 1.f;
-  if (FP8) {  // ALU-converted tiles hold x * 2^-8 (see e4m3x4_to_f16x4_s8); cvt ones hold x
-    const float f = hw ? 1.f : 256.f;
-    a.scale_log2 *= (p->k_scale > 0.f ? p->k_scale : 1.f) * f;
-    a.out_scale = (p->v_scale > 0.f ? p->v_scale : 1.f) * f;
+  if (FP8) {  // K = e4m3 * k_scale, V = e4m3 * v_scale
+    a.scale_log2 *= (p->k_scale > 0.f ? p->k_scale : 1.f);
+    a.out_scale = (p->v_scale > 0.f ? p->v_scale : 1.f);
   }
   kern<<<ctas, C::NTHREADS, C::SMEM_BYTES, stream>>>(mq, mk, mv, a);
   cudaError_t e = cudaGetLastError();
@@ -394,12 +380,13 @@ struct FlatEntry {
   FlatLauncher fn;
   int smem;
 };
-#define FF(G, NS) {G, NS, false, &launch_flat<G, NS, false>, b200::FlatCfg<G, NS, 0>::SMEM_BYTES}
-#define F8(G, NS) {G, NS, true, &launch_flat<G, NS, true>, b200::FlatCfg<G, NS, 1>::SMEM_BYTES}
+#define FF(G, NS) {G, NS, false, &launch_flat<G, NS, false>, b200::FlatCfg<G, NS, false>::SMEM_BYTES}
+#define F8(G, NS) {G, NS, true, &launch_flat<G, NS, true>, b200::FlatCfg<G, NS, true>::SMEM_BYTES}
 const FlatEntry kFlat[] = {FF(1, 3), FF(1, 4), FF(1, 5), FF(1, 6), FF(2, 3), FF(2, 4), FF(2, 5), FF(2, 6),
                            FF(4, 3), FF(4, 4), FF(4, 5), FF(8, 3), FF(8, 4),
-                           // fp8 e4m3 KV: num_stages = depth of the 16-KB fp8 staging ring
-                           F8(1, 4), F8(1, 6), F8(2, 4), F8(2, 6), F8(4, 3), F8(4, 4), F8(4, 5), F8(8, 3)};
+                           // fp8 e4m3 KV: num_stages = depth of the ring of 16-KB pages
+                           F8(1, 4), F8(1, 6), F8(1, 8), F8(2, 4), F8(2, 6), F8(2, 8), F8(4, 4), F8(4, 6),
+                           F8(4, 8), F8(8, 4), F8(8, 6)};
 #undef FF
 #undef F8
 
@@ -718,7 +705,17 @@ int b200attn_debug_umma_rate(int mode, int iters, int ctas, long long* out_dev, 
 
 int b200attn_selftest_umma(int mode, const void* a, const void* b, float* d, void* stream) {
   g_err[0] = 0;
-  if (mode < 0 || mode > 3 || !a || !b || !d) return fail(B200ATTN_BAD_ARGS, "selftest args");
+  if (mode < 0 || mode > 5 || !a || !b || !d) return fail(B200ATTN_BAD_ARGS, "selftest args");
+  if (mode >= 4) {
+    const int smem = 2 * 128 * 128 + 16 + 1024;
+    cudaError_t ea = cudaFuncSetAttribute(b200::umma_selftest_fp8_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (ea != cudaSuccess) return cuda_fail(ea, "cudaFuncSetAttribute(selftest fp8)");
+    b200::umma_selftest_fp8_kernel<<<1, 128, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const uint8_t*>(a), reinterpret_cast<const uint8_t*>(b), d, mode);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? B200ATTN_OK : cuda_fail(e, "selftest fp8 launch");
+  }
   cudaError_t ea = cudaFuncSetAttribute(b200::umma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         b200::kSelftestSmem);
   if (ea != cudaSuccess) return cuda_fail(ea, "cudaFuncSetAttribute(selftest)");

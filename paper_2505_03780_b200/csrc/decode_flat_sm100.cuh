@@ -19,11 +19,12 @@
 // (cta + seq) and K3' (flat_combine_kernel) merges them.
 //
 // FP8 = true (e4m3 KV cache, per-tensor k_scale / v_scale — vLLM's FP8_PER_TENSOR semantics):
-// TMA streams each 16-KB fp8 page into a staging ring (NSTAGE deep); four converter warps turn
-// it into an fp16 SW128 operand tile (exact, values x 2^-8; a 3-deep operand ring) and retype Q
-// bf16 -> fp16 in place; the MMAs run kind::f16 with fp16 P.  2^8 * k_scale is folded into the
-// softmax scale and 2^8 * v_scale into the output scale, so HBM traffic halves and nothing else
-// changes.
+// the pages feed tcgen05 kind::f8f6f4 MMAs straight from their TMA tiles (one 16-KB SW128 box
+// per page; V as the MN-major A operand of PV) — no conversion pass.  The bf16-precision side
+// of each product is split into two e4m3 terms, hi = e4m3(x) and lo = e4m3(16 (x - hi)), stacked
+// along N: Q (scaled per q head by a power of two into e4m3 range) for QK^T, and P (scaled by
+// 2^4, with the lazy-max threshold at 4 so P*16 <= 256) for PV.  S = S_hi + S_lo / 16 and
+// O = O_hi + O_lo / 16 recover ~2^-8 relative precision, i.e. bf16-level operands.
 #pragma once
 #include "sm100_common.cuh"
 
@@ -39,80 +40,84 @@ struct FlatDecodeArgs {
   int32_t batch;
   int32_t block_size;
   int32_t max_blocks;
-  float scale_log2;  // softmax_scale * log2(e)  (fp8: * k_scale * 2^8)
-  float out_scale;   // 1                        (fp8: v_scale * 2^8)
+  float scale_log2;  // softmax_scale * log2(e)  (fp8: * k_scale)
+  float out_scale;   // 1                        (fp8: v_scale)
 };
 
-#ifndef B200_FP8_CONV_WARPS
-#define B200_FP8_CONV_WARPS 8
-#endif
-
-template <int G, int NSTAGE, int KVM = 0>  // KVM: 0 bf16 cache, 1 fp8 (ALU bit conversion), 2 fp8 (cvt.f16x2.e4m3x2)
+template <int G, int NSTAGE, bool FP8 = false>
 struct FlatCfg {
-  static constexpr bool FP8 = KVM != 0;
   static constexpr int D = 128, HKV = 8, TT = 16, ROWS = 128;
   static constexpr int NQ = 8 * G;
-  static constexpr int NP = NQ < 16 ? 16 : NQ;  // MMA N
-  // fp8 -> fp16 converter warps: 8 (the 128-register cap of 14 warps) unless the softmax needs
-  // more registers (G = 8 keeps 64 fp32 O accumulators per thread: 4 warps, 168 registers)
-  static constexpr int NCONV = FP8 ? (G >= 8 ? 4 : B200_FP8_CONV_WARPS) : 0;
-  static constexpr int NTHREADS = 192 + 32 * NCONV, TMA_WARP = 4, MMA_WARP = 5, CONV_WARP0 = 6;
-  static constexpr int SLOT = ROWS * D * 2, HALF = ROWS * 128;
-  static constexpr int OPS = FP8 ? 3 : NSTAGE;   // MMA operand ring (bf16 / fp16 tiles)
-  static constexpr int NSTG = FP8 ? NSTAGE : 0;  // fp8 staging ring (raw pages)
-  static constexpr int NSTG_DIV = NSTG > 0 ? NSTG : 1;  // divisor for ring arithmetic (bf16: dead code)
-  static constexpr int STG_SLOT = ROWS * D;      // one fp8 page of 8 kv heads x 16 tokens
-  static constexpr int QB = NP * 256, QHALF = NP * 128;
-  static constexpr int PB = NP * 256, PHALF = NP * 128;
+  static constexpr int NP = NQ < 16 ? 16 : NQ;  // MMA N per operand term
+  static constexpr int NT = FP8 ? 2 : 1;        // terms stacked along N (hi, lo)
+  static constexpr int NTHREADS = 192, TMA_WARP = 4, MMA_WARP = 5;
+  static constexpr int SLOT = ROWS * D * (FP8 ? 1 : 2), HALF = ROWS * 128;  // one K or V page tile
+  static constexpr int QB = NP * 256, QHALF = NP * 128;  // bf16 Q tile (as TMA loads it)
+  static constexpr int Q8B = 2 * NP * 128;               // fp8 [Q_hi; Q_lo] tile (FP8)
+  static constexpr int PB = FP8 ? 2 * NP * 128 : NP * 256, PHALF = NP * 128;
   static constexpr int MAXB = 1024;
   static constexpr int OFF_KV = 0;
-  static constexpr int OFF_STG = OFF_KV + OPS * SLOT;
-  static constexpr int OFF_Q = OFF_STG + NSTG * STG_SLOT;
-  static constexpr int OFF_P = OFF_Q + 2 * QB;
-  static constexpr int OFF_ALPHA = OFF_P + 2 * PB;     // [NP] f32 rescale factors + int32 flags[2][4]
-  static constexpr int OFF_ML = OFF_ALPHA + 3 * NP * 4;  // [2][NP] f32
+  static constexpr int OFF_Q = OFF_KV + NSTAGE * SLOT;
+  static constexpr int OFF_Q8 = OFF_Q + 2 * QB;
+  static constexpr int OFF_P = OFF_Q8 + (FP8 ? 2 * Q8B : 0);
+  static constexpr int OFF_ALPHA = OFF_P + 2 * PB;       // [NP] f32 rescale factors + int32 flags[2][4]
+  static constexpr int OFF_QS = OFF_ALPHA + 2 * NP * 4;  // [2][NP] f32 per-q-head Q scales (FP8)
+  static constexpr int OFF_ML = OFF_QS + 2 * NP * 4;     // [2][NP] f32
   static constexpr int OFF_CU = OFF_ML + 2 * NP * 4;     // [MAXB + 1] i32
   static constexpr int OFF_BAR = (OFF_CU + (MAXB + 1) * 4 + 7) & ~7;
-  static constexpr int NUM_BARS = 4 + 2 * OPS + 8 + 2 * NSTG + 2;
+  static constexpr int NUM_BARS = 4 + 2 * NSTAGE + 8 + 2;
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
-  static constexpr uint32_t TMEM_COLS = (4 * NP <= 64) ? 64 : (4 * NP <= 128 ? 128 : 256);
-  __host__ __device__ static constexpr uint32_t S_COL(int i) { return (i & 1) * NP; }  // per tile
-  __host__ __device__ static constexpr uint32_t O_COL(int k) { return 2 * NP + (k & 1) * NP; }  // per segment
+  static constexpr int TCOLS = 4 * NT * NP;  // S[2] + O[2], NT terms each
+  static constexpr uint32_t TMEM_COLS = TCOLS <= 64 ? 64 : (TCOLS <= 128 ? 128 : (TCOLS <= 256 ? 256 : 512));
+  __host__ __device__ static constexpr uint32_t S_COL(int i) { return (i & 1) * NT * NP; }                // per tile
+  __host__ __device__ static constexpr uint32_t O_COL(int k) { return 2 * NT * NP + (k & 1) * NT * NP; }  // per segment
+  static constexpr float LAZY = FP8 ? 4.0f : 8.0f;  // log2 headroom before the running max moves
 };
 
 __device__ __forceinline__ int flat_cta_of(int t, int ctas, int ntiles) {
   return static_cast<int>(((static_cast<long long>(t) + 1) * ctas - 1) / ntiles);
 }
 
-template <int G, int NSTAGE, int KVM = 0>
-__global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
+// byte offset of element (row, col) of a [rows][128 B] SW128 tile (16-byte chunk ^ row % 8)
+__device__ __forceinline__ uint32_t sw128_b(int row, int col) {
+  return row * 128 + ((((col >> 4) ^ (row & 7))) << 4) + (col & 15);
+}
+
+// (x0, x1) -> e4m3 hi bytes and lo bytes of the split x ~ hi + lo / 16 (satfinite, RN)
+__device__ __forceinline__ void e4m3_split2(float x0, float x1, uint16_t& hi, uint16_t& lo) {
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(x1), "f"(x0));
+  uint32_t h16;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h16) : "h"(hi));
+  const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h16));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"((x1 - hf.y) * 16.f), "f"((x0 - hf.x) * 16.f));
+}
+
+template <int G, int NSTAGE, bool FP8 = false>
+__global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
     decode_flat_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
                        const __grid_constant__ CUtensorMap tmap_v, const FlatDecodeArgs args) {
-  using C = FlatCfg<G, NSTAGE, KVM>;
-  constexpr int NQ = C::NQ, NP = C::NP, D = C::D, OPS = C::OPS;
-  constexpr bool FP8 = C::FP8;
-  static_assert(!FP8 || C::NSTG >= 3, "fp8 staging ring must be >= 3 deep (K runs one tile ahead of V)");
+  using C = FlatCfg<G, NSTAGE, FP8>;
+  constexpr int NQ = C::NQ, NP = C::NP, D = C::D, NT = C::NT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sKV = smem + C::OFF_KV;
-  uint8_t* sSTG = smem + C::OFF_STG;
   uint8_t* sQ = smem + C::OFF_Q;
+  uint8_t* sQ8 = smem + C::OFF_Q8;
   uint8_t* sP = smem + C::OFF_P;
   float* alpha_s = reinterpret_cast<float*>(smem + C::OFF_ALPHA);
+  float* qs_s = reinterpret_cast<float*>(smem + C::OFF_QS);
   float* ml_s = reinterpret_cast<float*>(smem + C::OFF_ML);
   int32_t* cu = reinterpret_cast<int32_t*>(smem + C::OFF_CU);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* q_full = bars;           // [2]
-  uint64_t* q_empty = bars + 2;      // [2]
-  uint64_t* kv_full = bars + 4;      // [OPS] operand tile ready for the MMA
-  uint64_t* kv_empty = kv_full + OPS;
-  uint64_t* s_full = kv_empty + OPS;  // [2]
+  uint64_t* q_full = bars;       // [2] bf16 Q landed (TMA)
+  uint64_t* q_empty = bars + 2;  // [2]
+  uint64_t* kv_full = bars + 4;  // [NSTAGE]
+  uint64_t* kv_empty = kv_full + NSTAGE;
+  uint64_t* s_full = kv_empty + NSTAGE;  // [2]
   uint64_t* p_full = s_full + 2;
   uint64_t* o_full = p_full + 2;
   uint64_t* o_empty = o_full + 2;
-  uint64_t* stg_full = o_empty + 2;  // [NSTG] fp8 page landed (FP8 only)
-  uint64_t* stg_empty = stg_full + C::NSTG;
-  uint64_t* q_conv = stg_empty + C::NSTG;  // [2] Q retyped to fp16 (FP8 only)
+  uint64_t* q_conv = o_empty + 2;  // [2] fp8 Q split ready (FP8)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS);
   const int warp = warp_id(), lane = lane_id();
   const int B = args.batch;
@@ -133,31 +138,22 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
       carry += __shfl_sync(0xffffffffu, v, 31);
     }
   }
-  // zero Q (padded rows) and P^T (block-diagonal zeros) once
-  for (int i = threadIdx.x; i < (2 * C::QB + 2 * C::PB) / 16; i += C::NTHREADS)
+  // zero Q (padded rows), the fp8 Q split and P^T (block-diagonal zeros) once
+  for (int i = threadIdx.x; i < (C::OFF_ALPHA - C::OFF_Q) / 16; i += C::NTHREADS)
     reinterpret_cast<uint4*>(sQ)[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 32) {
-    mbar_init(&q_full[0], 1);
-    mbar_init(&q_full[1], 1);
-    mbar_init(&q_empty[0], 1);
-    mbar_init(&q_empty[1], 1);
-    for (int i = 0; i < OPS; ++i) {
-      mbar_init(&kv_full[i], FP8 ? C::NCONV : 1);
-      mbar_init(&kv_empty[i], 1);
-    }
-    for (int i = 0; i < C::NSTG; ++i) {
-      mbar_init(&stg_full[i], 1);
-      mbar_init(&stg_empty[i], C::NCONV);
-    }
-    if (FP8) {
-      mbar_init(&q_conv[0], C::NCONV);
-      mbar_init(&q_conv[1], C::NCONV);
-    }
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&q_conv[i], 128);
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 128);
       mbar_init(&o_full[i], 1);
       mbar_init(&o_empty[i], 128);
+    }
+    for (int i = 0; i < NSTAGE; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
     }
     fence_barrier_init();
   }
@@ -216,16 +212,7 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
           const int pg = __shfl_sync(0xffffffffu, page, j);
           const int tok = (base + j - tile0) * C::TT;
           const int row = pg * bs + (tok & (bs - 1));
-          if (FP8 && lane == 0) {
-#pragma unroll
-            for (int kv = 0; kv < 2; ++kv, ++it) {
-              const int slot = it % C::NSTG_DIV;
-              mbar_wait(&stg_empty[slot], ((it / C::NSTG_DIV) & 1) ^ 1);
-              mbar_arrive_expect_tx(&stg_full[slot], C::STG_SLOT);
-              tma_load_3d_hint(sSTG + slot * C::STG_SLOT, kv ? &tmap_v : &tmap_k, &stg_full[slot], 0, row, 0,
-                               stream_once);
-            }
-          } else if (lane == 0) {
+          if (lane == 0) {
 #pragma unroll
             for (int kv = 0; kv < 2; ++kv, ++it) {
               const int slot = it % NSTAGE;
@@ -234,7 +221,7 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
               uint8_t* dst = sKV + slot * C::SLOT;
               const CUtensorMap* map = kv ? &tmap_v : &tmap_k;
               tma_load_3d_hint(dst, map, &kv_full[slot], 0, row, 0, stream_once);
-              tma_load_3d_hint(dst + C::HALF, map, &kv_full[slot], 64, row, 0, stream_once);
+              if (!FP8) tma_load_3d_hint(dst + C::HALF, map, &kv_full[slot], 64, row, 0, stream_once);
             }
           }
         }
@@ -244,131 +231,71 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
   } else if (warp == C::MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer (whole warp, one elected lane issues)
     {
-      constexpr uint32_t IDESC_QK = FP8 ? idesc_f16_f32(C::ROWS, NP, false, false) : idesc_bf16_f32(C::ROWS, NP, false, false);
-      constexpr uint32_t IDESC_PV = FP8 ? idesc_f16_f32(D, NP, true, false) : idesc_bf16_f32(D, NP, true, false);
+      constexpr uint32_t IDESC_QK =
+          FP8 ? idesc_e4m3_f32(C::ROWS, NT * NP, false, false) : idesc_bf16_f32(C::ROWS, NP, false, false);
+      constexpr uint32_t IDESC_PV =
+          FP8 ? idesc_e4m3_f32(D, NT * NP, true, false) : idesc_bf16_f32(D, NP, true, false);
       const uint64_t k_desc = sdesc_sw128(smem_u32(sKV), 16, 1024);
-      const uint64_t v_desc = sdesc_sw128(smem_u32(sKV), C::HALF, 1024);
-      const uint64_t q_desc = sdesc_sw128(smem_u32(sQ), 16, 1024);
+      const uint64_t v_desc = sdesc_sw128(smem_u32(sKV), FP8 ? 16 : C::HALF, 1024);
+      const uint64_t q_desc = sdesc_sw128(smem_u32(FP8 ? sQ8 : sQ), 16, 1024);
       const uint64_t p_desc = sdesc_sw128(smem_u32(sP), 16, 1024);
-      // operand-ring positions: bf16 = TMA order K0 V0 K1 V1 ...; fp8 = MMA consumption order
-      // K0 K1 V0 K2 V1 ... V_{n-1} (the converters fill the ring in exactly this order)
-      const int n_tiles = T1 - T0;
-      auto kpos = [&](int i) { return FP8 ? (i == 0 ? 0 : 2 * i - 1) : 2 * i; };
-      auto vpos = [&](int i) { return FP8 ? min(2 * i + 2, 2 * n_tiles - 1) : 2 * i + 1; };
       auto qk = [&](int i, int qb) {
-        const int idx = kpos(i), slot = idx % OPS;
-        mbar_wait(&kv_full[slot], (idx / OPS) & 1);
+        const int idx = 2 * i, slot = idx % NSTAGE;
+        mbar_wait(&kv_full[slot], (idx / NSTAGE) & 1);
         tc_fence_after();
-        const uint64_t kb = k_desc + ((slot * C::SLOT) >> 4), qa = q_desc + ((qb * C::QB) >> 4);
-        umma_ss_k128<2, C::HALF / 16, 2, C::QHALF / 16>(tmem + C::S_COL(i), kb, qa, IDESC_QK, 0u);
+        const uint64_t kb = k_desc + ((slot * C::SLOT) >> 4);
+        if constexpr (FP8) {
+          // K = 32 bytes per step along the 128-byte rows of K and of [Q_hi; Q_lo]
+          umma_f8_ss_k128<2, 2>(tmem + C::S_COL(i), kb, q_desc + ((qb * C::Q8B) >> 4), IDESC_QK, 0u);
+        } else {
+          umma_ss_k128<2, C::HALF / 16, 2, C::QHALF / 16>(tmem + C::S_COL(i), kb, q_desc + ((qb * C::QB) >> 4),
+                                                          IDESC_QK, 0u);
+        }
         umma_commit_w(&s_full[i & 1]);
         umma_commit_w(&kv_empty[slot]);
       };
       // PV of tile i accumulates into segment seg's O buffer (fresh on the segment's first tile,
       // which first waits for the epilogue of segment seg-2 to release the buffer)
       auto pv = [&](int i, int seg, bool first) {
-        const int idx = vpos(i), slot = idx % OPS;
-        mbar_wait(&kv_full[slot], (idx / OPS) & 1);
+        const int idx = 2 * i + 1, slot = idx % NSTAGE;
+        mbar_wait(&kv_full[slot], (idx / NSTAGE) & 1);
         mbar_wait(&p_full[i & 1], (i >> 1) & 1);
         if (first && seg >= 2) mbar_wait(&o_empty[seg & 1], ((seg >> 1) - 1) & 1);
         tc_fence_after();
         const uint64_t vb = v_desc + ((slot * C::SLOT) >> 4), pb = p_desc + (((i & 1) * C::PB) >> 4);
-        umma_ss_k128<128, 512, 2, C::PHALF / 16>(tmem + C::O_COL(seg), vb, pb, IDESC_PV, first ? 0u : 1u);
+        if constexpr (FP8) {
+          // V^T is the MN-major A operand: 32 (head, token) rows = 4096 B per K step
+          umma_f8_ss_k128<((32 * 128) >> 4), 2>(tmem + C::O_COL(seg), vb, pb, IDESC_PV, first ? 0u : 1u);
+        } else {
+          umma_ss_k128<128, 512, 2, C::PHALF / 16>(tmem + C::O_COL(seg), vb, pb, IDESC_PV, first ? 0u : 1u);
+        }
         umma_commit_w(&o_full[i & 1]);  // PV(i) lands: o_full[i & 1], phase (i >> 1) & 1
         umma_commit_w(&kv_empty[slot]);
       };
+      // Order: QK(i) then PV(i-1) inside a segment (the softmax of tile i overlaps PV(i-1)); at a
+      // segment boundary the previous segment's last PV goes first, so its epilogue never waits on
+      // the next segment's Q (which, for fp8, the softmax warps themselves prepare).
       int i = 0, k = 0, b = b_first, pk = 0;
       bool pfirst = false;
       for (int t = T0; t < T1; ++k) {
         while (cu[b + 1] <= t) ++b;
         const int seg_end = min(T1, cu[b + 1]), seg_t0 = t;
+        if (i >= 1) pv(i - 1, pk, pfirst);
         mbar_wait(FP8 ? &q_conv[k & 1] : &q_full[k & 1], (k >> 1) & 1);
         for (; t < seg_end; ++t, ++i) {
           qk(i, k & 1);
           if (t == seg_end - 1) umma_commit_w(&q_empty[k & 1]);
-          if (i >= 1) pv(i - 1, pk, pfirst);
+          if (t != seg_t0) pv(i - 1, pk, pfirst);
           pk = k;
           pfirst = (t == seg_t0);
         }
       }
       pv(i - 1, pk, pfirst);
     }
-  } else if (FP8 && warp >= C::CONV_WARP0) {
-    // ------------------------------------------------------------ fp8 -> fp16 converters (FP8 only)
-    const int ct = threadIdx.x - 32 * C::CONV_WARP0;
-    const uint32_t stg0 = smem_u32(sSTG), kv0 = smem_u32(sKV);
-    const int n_tiles = T1 - T0;
-    // staging entry sidx (TMA order: K_i = 2i, V_i = 2i+1) -> operand position opos (MMA order)
-    // thread ct converts the 16-byte chunk c = ct % 8 of rows r0 + j*CT/8 (row = head*16 + token,
-    // 16 d per chunk); CT/8 is a multiple of 8, so the swizzle phase row % 8 is per-thread constant
-    constexpr int CT = C::NCONV > 0 ? 32 * C::NCONV : 32;
-    static_assert(!FP8 || (1024 % CT == 0 && (CT / 8) % 8 == 0), "converter thread mapping");
-    const int c = ct & 7, r0 = ct >> 3, sw = r0 & 7, x0 = (2 * c) & 7;
-    const uint32_t src_off = r0 * 128 + c * 16;
-    const uint32_t line_off = (c >> 2) * C::HALF + r0 * 128;
-    const uint32_t d_lo = line_off + ((x0 ^ sw) << 4), d_hi = line_off + (((x0 + 1) ^ sw) << 4);
-    auto convert = [&](int sidx, int opos) {
-      const int slot = sidx % C::NSTG_DIV, oslot = opos % OPS;
-      mbar_wait(&stg_full[slot], (sidx / C::NSTG_DIV) & 1);
-      mbar_wait(&kv_empty[oslot], ((opos / OPS) & 1) ^ 1);
-      const uint32_t src = stg0 + slot * C::STG_SLOT + src_off, dst = kv0 + oslot * C::SLOT;
-#pragma unroll
-      for (int j = 0; j < 1024 / CT; ++j) {
-        const uint32_t rstep = j * (CT / 8) * 128;
-        const uint4 w = ld_shared_v4(src + rstep);
-        uint32_t f[8];
-        if constexpr (KVM == 2) {
-          e4m3x4_to_f16x4_hw(w.x, f[0], f[1]);
-          e4m3x4_to_f16x4_hw(w.y, f[2], f[3]);
-          e4m3x4_to_f16x4_hw(w.z, f[4], f[5]);
-          e4m3x4_to_f16x4_hw(w.w, f[6], f[7]);
-        } else {
-          e4m3x4_to_f16x4_s8(w.x, f[0], f[1]);
-          e4m3x4_to_f16x4_s8(w.y, f[2], f[3]);
-          e4m3x4_to_f16x4_s8(w.z, f[4], f[5]);
-          e4m3x4_to_f16x4_s8(w.w, f[6], f[7]);
-        }
-        // d [16c, 16c+16) -> 64-col half c/4, 16-B chunks 2(c%4) and 2(c%4)+1, SW128 (chunk ^ row%8)
-        const uint32_t line = dst + rstep;
-        if (c < 4) {  // even chunks first for c < 4, odd first for c >= 4: no bank conflicts
-          st_shared_v4(line + d_lo, f[0], f[1], f[2], f[3]);
-          st_shared_v4(line + d_hi, f[4], f[5], f[6], f[7]);
-        } else {
-          st_shared_v4(line + d_hi, f[4], f[5], f[6], f[7]);
-          st_shared_v4(line + d_lo, f[0], f[1], f[2], f[3]);
-        }
-      }
-      fence_proxy_async_smem();  // this thread's operand writes -> async proxy
-      __syncwarp();
-      if (lane == 0) {  // one arrival per converter warp
-        mbar_arrive(&stg_empty[slot]);
-        mbar_arrive(&kv_full[oslot]);
-      }
-    };
-    int i = 0, k = 0, b = b_first;
-    for (int t = T0; t < T1; ++k) {
-      while (cu[b + 1] <= t) ++b;
-      const int seg_end = min(T1, cu[b + 1]);
-      mbar_wait(&q_full[k & 1], (k >> 1) & 1);
-      uint32_t* qw = reinterpret_cast<uint32_t*>(sQ + (k & 1) * C::QB);
-      for (int x = ct; x < NQ * 64; x += 32 * C::NCONV) {  // rows >= NQ are zero padding (0 -> 0)
-        const int r = x >> 6, h = (x >> 5) & 1, w = x & 31;  // row, 64-col half, word in the 128-B line
-        qw[h * (C::QHALF / 4) + r * 32 + w] = bf16x2_to_f16x2(qw[h * (C::QHALF / 4) + r * 32 + w]);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&q_conv[k & 1]);
-#pragma unroll 1
-      for (; t < seg_end; ++t, ++i) {
-        convert(2 * i, i == 0 ? 0 : 2 * i - 1);                          // K_i
-        if (i >= 1) convert(2 * i - 1, min(2 * i, 2 * n_tiles - 1));   // V_{i-1}
-      }
-    }
-    convert(2 * n_tiles - 1, 2 * n_tiles - 1);  // V_{n-1}
   } else {
     // ------------------------------------------------------------ softmax + epilogue
     // O^T accumulates in TMEM across a segment's tiles (PV with acc = 1).  Exponentials use the
-    // running max m_run, which only moves when a score exceeds it by more than 8 (log2 units,
+    // running max m_run, which only moves when a score exceeds it by more than LAZY (log2 units,
     // FA4's lazy rescale): then, and on a segment's first tile, the CTA takes the slow path —
     // exact per-head max (16-lane shuffles), alpha to smem, and once PV(i-1) has landed every
     // thread rescales its O^T row in TMEM.  The common tile is a vote, G exp2 and G P stores.
@@ -378,11 +305,12 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
     const uint32_t lane_base = static_cast<uint32_t>(warp << 5) << 16;
     const uint32_t col_base = static_cast<uint32_t>(warp * 2 * G);
     const float sl2 = args.scale_log2;
-    const uint32_t p_base = smem_u32(sP) + (row >> 6) * C::PHALF + (row & 7) * 2;
+    const uint32_t p_base = smem_u32(sP) + (row >> 6) * C::PHALF + (row & 7) * 2;  // bf16 P^T
     const int rchunk = (row & 63) >> 3;
     volatile int* flags = reinterpret_cast<volatile int*>(alpha_s + NP);  // [2][4] per-warp votes
+    constexpr float LAZY = C::LAZY;
 
-    float m_run[G], l_part[G];
+    float m_run[G], l_part[G], fac[G];
     int i = 0, b = b_first;
     for (int t = T0, k = 0; t < T1; ++k) {
       while (cu[b + 1] <= t) ++b;
@@ -390,6 +318,54 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
       const int tile0 = cu[b];
       const int len = args.seq_lens[b];
       const bool complete = (t == tile0) && (seg_end == cu[b + 1]);
+      if constexpr (FP8) {
+        // ---- Q (bf16, SW128 halves) -> [Q_hi; Q_lo] e4m3 rows, scaled per q head by 2^e so the
+        // largest |q| lands in [128, 256); TPR threads per q head, 8-element chunks
+        constexpr int TPR = 128 / NQ, CPT = 16 / TPR;  // threads per row, 8-wide chunks per thread
+        mbar_wait(&q_full[k & 1], (k >> 1) & 1);
+        const int qh = row / TPR, part = row % TPR;
+        const uint8_t* qsrc = sQ + (k & 1) * C::QB;
+        uint8_t* qdst = sQ8 + (k & 1) * C::Q8B;
+        uint4 v[CPT];
+        float amax = 0.f;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          const int ch = part * CPT + c;  // 8-element chunk of the 128-wide row: half ch/8, chunk ch%8
+          v[c] = *reinterpret_cast<const uint4*>(qsrc + (ch >> 3) * C::QHALF + qh * 128 +
+                                                  (((ch & 7) ^ (qh & 7)) << 4));
+          const uint32_t w[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            amax = fmaxf(amax, fmaxf(fabsf(__uint_as_float(w[e] << 16)), fabsf(__uint_as_float(w[e] & 0xFFFF0000u))));
+        }
+#pragma unroll
+        for (int off = 1; off < TPR; off <<= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+        // power-of-two scale: exact, max |q| * qs in [128, 256)
+        const float qscale = amax > 0.f ? exp2f(7.f - floorf(__log2f(amax))) : 1.f;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          const int ch = part * CPT + c, col = ch * 8;
+          const uint32_t w[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+          uint16_t hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            e4m3_split2(__uint_as_float(w[e] << 16) * qscale, __uint_as_float(w[e] & 0xFFFF0000u) * qscale, hi[e],
+                        lo[e]);
+          const uint2 hv = make_uint2(hi[0] | (uint32_t(hi[1]) << 16), hi[2] | (uint32_t(hi[3]) << 16));
+          const uint2 lv = make_uint2(lo[0] | (uint32_t(lo[1]) << 16), lo[2] | (uint32_t(lo[3]) << 16));
+          *reinterpret_cast<uint2*>(qdst + sw128_b(qh, col)) = hv;
+          *reinterpret_cast<uint2*>(qdst + sw128_b(NP + qh, col)) = lv;
+        }
+        if (part == 0) qs_s[(k & 1) * NP + qh] = 1.f / qscale;
+        fence_proxy_async_smem();
+        mbar_arrive(&q_conv[k & 1]);
+        named_bar_sync(1, 128);  // qs_s visible
+#pragma unroll
+        for (int g = 0; g < G; ++g) fac[g] = sl2 * qs_s[(k & 1) * NP + h * G + g];
+      } else {
+#pragma unroll
+        for (int g = 0; g < G; ++g) fac[g] = sl2;
+      }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         m_run[g] = -INFINITY;
@@ -400,17 +376,28 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
         const int sb = i & 1;
         mbar_wait(&s_full[sb], (i >> 1) & 1);
         tc_fence_after();
-        uint32_t sv[2 * G];
-        tmem_ld_cols<2 * G>(tmem + lane_base + C::S_COL(i) + col_base, sv);
         const int tok = (t - tile0) * C::TT + t16;
         const bool valid = tok < len;
         float x[G];
         bool need = false;
+        {
+          uint32_t sv[2 * G];
+          tmem_ld_cols<2 * G>(tmem + lane_base + C::S_COL(i) + col_base, sv);
+          if constexpr (FP8) {
+            uint32_t sl[2 * G];
+            tmem_ld_cols<2 * G>(tmem + lane_base + C::S_COL(i) + NP + col_base, sl);
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          x[g] = valid ? __uint_as_float(upper ? sv[G + g] : sv[g]) * sl2 : -INFINITY;
-          need |= x[g] > m_run[g] + 8.0f;
+            for (int g = 0; g < G; ++g)
+              x[g] = valid ? fmaf(__uint_as_float(upper ? sl[G + g] : sl[g]), 0.0625f,
+                                  __uint_as_float(upper ? sv[G + g] : sv[g])) * fac[g]
+                           : -INFINITY;
+          } else {
+#pragma unroll
+            for (int g = 0; g < G; ++g) x[g] = valid ? __uint_as_float(upper ? sv[G + g] : sv[g]) * fac[g] : -INFINITY;
+          }
         }
+#pragma unroll
+        for (int g = 0; g < G; ++g) need |= x[g] > m_run[g] + LAZY;
         const bool warp_need = __any_sync(0xffffffffu, need);
         if (lane == 0) flags[sb * 4 + warp] = warp_need;
         named_bar_sync(1, 128);
@@ -422,7 +409,7 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
 #pragma unroll
             for (int off = 1; off < 16; off <<= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
             float alpha = 1.f;
-            if (mt > m_run[g] + 8.0f) {
+            if (mt > m_run[g] + LAZY) {
               alpha = (m_run[g] == -INFINITY) ? 0.f : fast_exp2(m_run[g] - mt);
               m_run[g] = mt;
               l_part[g] *= alpha;
@@ -433,43 +420,63 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
           if (i > seg_i0) {  // O holds tiles seg_i0 .. i-1: rescale once PV(i-1) has landed
             mbar_wait(&o_full[(i - 1) & 1], ((i - 1) >> 1) & 1);
             tc_fence_after();
-            uint32_t r[NQ];
-            tmem_ld_cols<NQ>(tmem + lane_base + C::O_COL(k), r);
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) * alpha_s[q]);
-            tmem_st_cols<NQ>(tmem + lane_base + C::O_COL(k), r);
+            for (int term = 0; term < NT; ++term) {
+              uint32_t r[NQ];
+              tmem_ld_cols<NQ>(tmem + lane_base + C::O_COL(k) + term * NP, r);
+#pragma unroll
+              for (int q = 0; q < NQ; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) * alpha_s[q]);
+              tmem_st_cols<NQ>(tmem + lane_base + C::O_COL(k) + term * NP, r);
+            }
             tmem_wait_st();
           }
         }
-        const uint32_t pb = p_base + sb * C::PB;
+        uint8_t* pt = sP + sb * C::PB;
+        if constexpr (FP8) {
+          // P^T as [P_hi; P_lo] e4m3 rows (row = q head, column = this thread's (head, token))
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const float mu = (m_run[g] == -INFINITY) ? 0.f : m_run[g];
-          const float p = fast_exp2(x[g] - mu);  // x = -inf (invalid / masked) -> 0
-          l_part[g] += p;
-          const int qh = h * G + g;
-          uint16_t pbits;
-          if constexpr (FP8) {
-            const __half p16 = __float2half_rn(p);
-            pbits = *reinterpret_cast<const uint16_t*>(&p16);
-          } else {
-            const __nv_bfloat16 p16 = __float2bfloat16_rn(p);
-            pbits = *reinterpret_cast<const uint16_t*>(&p16);
+          for (int g = 0; g < G; g += 2) {
+            float p2[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const float mu = (m_run[g + u] == -INFINITY) ? 0.f : m_run[g + u];
+              p2[u] = (g + u < G) ? fast_exp2(x[g + u] - mu) : 0.f;
+              if (g + u < G) l_part[g + u] += p2[u];
+            }
+            uint16_t hi, lo;
+            e4m3_split2(p2[0] * 16.f, p2[1] * 16.f, hi, lo);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              if (g + u >= G) break;
+              const int qh = h * G + g + u;
+              pt[sw128_b(qh, row)] = static_cast<uint8_t>(u ? hi >> 8 : hi & 0xFF);
+              pt[sw128_b(NP + qh, row)] = static_cast<uint8_t>(u ? lo >> 8 : lo & 0xFF);
+            }
           }
-          asm volatile("st.shared.b16 [%0], %1;" ::"r"(pb + qh * 128 + ((rchunk ^ (qh & 7)) << 4)), "h"(pbits)
-                       : "memory");
+        } else {
+          const uint32_t pb = p_base + sb * C::PB;
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float mu = (m_run[g] == -INFINITY) ? 0.f : m_run[g];
+            const float p = fast_exp2(x[g] - mu);  // x = -inf (invalid / masked) -> 0
+            l_part[g] += p;
+            const int qh = h * G + g;
+            const __nv_bfloat16 p16 = __float2bfloat16_rn(p);
+            asm volatile("st.shared.b16 [%0], %1;" ::"r"(pb + qh * 128 + ((rchunk ^ (qh & 7)) << 4)),
+                         "h"(*reinterpret_cast<const uint16_t*>(&p16))
+                         : "memory");
+          }
         }
-        if (KVM != 1 && !valid) {
-          // the page's tail slots past the sequence end hold arbitrary bytes: P = 0 there, but
-          // 0 * NaN would poison O, so zero this row of the V tile before PV reads it (the ALU
-          // fp8 conversion, KVM 1, cannot produce NaN/Inf and needs no zeroing)
-          const int vidx = FP8 ? min(2 * i + 2, 2 * (T1 - T0) - 1) : 2 * i + 1, vslot = vidx % OPS;
-          mbar_wait(&kv_full[vslot], (vidx / OPS) & 1);
+        if (!valid) {
+          // the page's tail slots past the sequence end hold arbitrary bytes (NaN included): P = 0
+          // there, but 0 * NaN would poison O, so zero this row of the V tile before PV reads it
+          const int vidx = 2 * i + 1, vslot = vidx % NSTAGE;
+          mbar_wait(&kv_full[vslot], (vidx / NSTAGE) & 1);
           uint4* vr = reinterpret_cast<uint4*>(sKV + vslot * C::SLOT + row * 128);
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             vr[c] = make_uint4(0, 0, 0, 0);
-            vr[C::HALF / 16 + c] = make_uint4(0, 0, 0, 0);
+            if (!FP8) vr[C::HALF / 16 + c] = make_uint4(0, 0, 0, 0);
           }
         }
         fence_proxy_async_smem();
@@ -494,6 +501,14 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, KVM>::NTHREADS, 1)
       tc_fence_after();
       uint32_t r[NQ];
       tmem_ld_cols<NQ>(tmem + lane_base + C::O_COL(k), r);
+      if constexpr (FP8) {
+        uint32_t rl[NQ];
+        tmem_ld_cols<NQ>(tmem + lane_base + C::O_COL(k) + NP, rl);
+        // O = (O_hi + O_lo / 16) / 16 (P was scaled by 16)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          r[q] = __float_as_uint(fmaf(__uint_as_float(rl[q]), 0.0625f, __uint_as_float(r[q])) * 0.0625f);
+      }
       tc_fence_before();
       mbar_arrive(&o_empty[k & 1]);
       named_bar_sync(1, 128);  // ml_s visible

@@ -150,6 +150,58 @@ __global__ void cache_append_fp8_kernel(const uint4* __restrict__ nk, const uint
   vc[dst] = bf16x8_to_e4m3x8(nv[src], inv_v);
 }
 
+// fp8 (e4m3) descriptor self-test: D[128x128] = A . B^T with 128-byte rows.
+//   mode 4: A [M=128][K=128] K-major, B [N=128][K=128] K-major
+//   mode 5: A given as [K=128][M=128] (MN-major), B K-major
+// Operands are byte tiles in the SW128 layout (16-byte chunk index ^ row % 8).
+__global__ void __launch_bounds__(128) umma_selftest_fp8_kernel(const uint8_t* A, const uint8_t* B, float* D,
+                                                                int mode) {
+  extern __shared__ uint8_t st_raw[];
+  uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(st_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sA + 128 * 128;
+  uint64_t& bar = *reinterpret_cast<uint64_t*>(sB + 128 * 128);
+  uint32_t& tslot = *reinterpret_cast<uint32_t*>(sB + 128 * 128 + 8);
+  const int tid = threadIdx.x;
+  auto sw = [](int r, int c) { return r * 128 + ((((c >> 4) ^ (r & 7)) << 4) | (c & 15)); };
+  for (int i = tid; i < 128 * 128; i += 128) {
+    const int r = i / 128, c = i % 128;
+    sA[sw(r, c)] = A[i];
+    sB[sw(r, c)] = B[i];
+  }
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (tid < 32) tmem_alloc(&tslot, 128);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (tid < 32) {
+    const uint32_t idesc = idesc_e4m3_f32(128, 128, mode == 5, false);
+    const uint64_t da = sdesc_sw128(smem_u32(sA), 16, 1024), db = sdesc_sw128(smem_u32(sB), 16, 1024);
+    // K step of 32: K-major operands advance 32 B within the row; MN-major A advances 32 rows
+    if (mode == 5) umma_f8_ss_k128<((32 * 128) >> 4), 2>(tmem, da, db, idesc, 0u);
+    else umma_f8_ss_k128<2, 2>(tmem, da, db, idesc, 0u);
+    umma_commit_w(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  const uint32_t taddr = tmem + (static_cast<uint32_t>((tid >> 5) << 5) << 16);
+  for (int c = 0; c < 4; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+    for (int j = 0; j < 32; ++j) D[tid * 128 + c * 32 + j] = __uint_as_float(r[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 128);
+  }
+}
+
 }  // namespace b200
 
 namespace b200 {

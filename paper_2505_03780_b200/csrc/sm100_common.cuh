@@ -150,6 +150,36 @@ __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// kind::f8f6f4 (e4m3 x e4m3 -> f32): D[tmem] (+)= A[smem] * B[smem]^T, K = 32 per instruction.
+__device__ __forceinline__ void umma_f8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Warp-convergent, K = 128 as 4 x K32 steps; A advances AS and B advances BS 16-byte units per step.
+template <int AS, int BS>
+__device__ __forceinline__ void umma_f8_ss_k128(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred e, p;\n\t.reg .b64 ta, tb;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t"
+      "setp.eq.u32 p, 0, 0;\n\t"
+      "add.s64 ta, %1, %5;\n\tadd.s64 tb, %2, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %7;\n\tadd.s64 tb, %2, %8;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %9;\n\tadd.s64 tb, %2, %10;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], ta, tb, %3, p;\n\t"
+      "}"
+      :: "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc), "n"(AS), "n"(BS), "n"(2 * AS), "n"(2 * BS),
+         "n"(3 * AS), "n"(3 * BS)
+      : "memory");
+}
+
 // Warp-convergent variants: the whole warp executes them (operands warp-uniform, so they stay
 // in uniform registers) and one elected lane issues — no divergent wrapper per MMA.
 __device__ __forceinline__ void umma_ss_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
@@ -383,6 +413,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N, bo
 
 // ------------------------------------------------------------- numerics
 // Blackwell packed fp32 pairs (FFMA2 / FADD2): two elements per issue slot.
+// Instruction descriptor, kind::f8f6f4: e4m3 x e4m3 -> f32 (a_format = b_format = 0 = E4M3).
+__host__ __device__ constexpr uint32_t idesc_e4m3_f32(uint32_t M, uint32_t N, bool a_mn, bool b_mn) {
+  return (1u << 4) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
 __device__ __forceinline__ void ffma2(float& y0, float& y1, float x0, float x1, float a, float b) {
   // (y0, y1) = (x0, x1) * a + b
   asm("{\n\t.reg .b64 x, s, c;\n\t"

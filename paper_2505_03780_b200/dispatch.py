@@ -29,8 +29,8 @@ DECODE_DEFAULT = {"num_splits": 0, "num_stages": 5, "TILE_N": 16}  # flat partit
 DECODE_SPLIT_DEFAULT = {"num_splits": 0, "num_stages": 4, "TILE_N": 128}  # any geometry
 
 _GEOM = ("num_q_heads", "num_kv_heads", "head_dim", "block_size", "causal", "kv_dtype")
-# fp8 KV (TILE_N=16 only): num_stages = fp8 staging-ring depth; deepest compiled variant per GQA group
-FP8_DECODE_STAGES = {1: 6, 2: 6, 4: 5, 8: 3}
+# fp8 KV (TILE_N=16 only): num_stages = depth of the ring of 16-KB pages; deepest compiled variant per GQA group
+FP8_DECODE_STAGES = {1: 8, 2: 8, 4: 8, 8: 6}
 
 _table = None
 

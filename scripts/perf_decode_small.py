@@ -26,7 +26,7 @@ for kv in ("bfloat16", "fp8_e4m3"):
     for B, S in ((1, 128), (1, 4096), (1, 32768), (4, 2048), (16, 1024), (64, 4096), (256, 8192)):
         d = W.make_decode(dict(W.C2, batch_size=B, seq_len=S, kv_dtype=kv), device="cuda")
         row = [f"{kv:9s} B={B:4d} S={S:6d}"]
-        for cfg in (dict(num_splits=0, num_stages=5 if kv == "bfloat16" else 5, TILE_N=16),
+        for cfg in (dict(num_splits=0, num_stages=5 if kv == "bfloat16" else 8, TILE_N=16),
                     dict(num_splits=0, num_stages=4, TILE_N=128)):
             try:
                 us = t(d, cfg)

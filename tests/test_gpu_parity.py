@@ -108,6 +108,18 @@ def test_umma_selftest(mode):
     assert (d.double() - ref).abs().max().item() < 1e-3
 
 
+@pytest.mark.parametrize("mode", [4, 5])
+def test_umma_selftest_fp8(mode):
+    """kind::f8f6f4 descriptors: e4m3 A (K-major, or MN-major given as [K][M]) x e4m3 B K-major."""
+    g = torch.Generator().manual_seed(mode)
+    a = (torch.randn(128, 128, generator=g) * 8).to(torch.float8_e4m3fn)
+    b = (torch.randn(128, 128, generator=g) * 8).to(torch.float8_e4m3fn)
+    d = A.selftest_umma(mode, a.view(torch.uint8).to(DEV), b.view(torch.uint8).to(DEV))
+    af, bf = a.double(), b.double()
+    ref = af @ bf.t() if mode == 4 else af.t() @ bf.t()
+    assert (d.double().cpu() - ref).abs().max().item() < 1e-2 * ref.abs().max().item()
+
+
 # ------------------------------------------------------------------ golden fixtures (upstream kernel)
 GOLDEN = sorted(glob.glob(str(ROOT / "tests" / "golden" / "*.npz")))
 
@@ -406,7 +418,7 @@ def run_decode_fp8(lens, Hq=32, cfg=None, seed=0, nan_tails=False):
     return out, ref, sdpa_decode_bf16(args[0], kb, vb, args[3], args[4])
 
 
-@pytest.mark.parametrize("hq,ns", [(8, 4), (8, 6), (16, 4), (16, 6), (32, 3), (32, 4), (32, 5), (64, 3)])
+@pytest.mark.parametrize("hq,ns", [(8, 4), (8, 6), (8, 8), (16, 4), (16, 6), (16, 8), (32, 4), (32, 6), (32, 8), (64, 4), (64, 6)])
 def test_decode_fp8_every_variant(hq, ns):
     out, ref, base = run_decode_fp8([1000, 333, 17, 1], Hq=hq, cfg=dcfg(0, ns, 16))
     check(f"decode fp8 hq={hq} stages={ns}", out, ref, base)

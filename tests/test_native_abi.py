@@ -114,7 +114,7 @@ def test_product_path_refuses_cpu_tensors():
 C2_Q, C2_CACHE = (64, 32, 128), (16384, 16, 8, 128)
 
 
-@pytest.mark.parametrize("hq,ns", [(8, 4), (8, 6), (16, 4), (16, 6), (32, 3), (32, 4), (32, 5), (64, 3)])
+@pytest.mark.parametrize("hq,ns", [(8, 4), (8, 6), (8, 8), (16, 4), (16, 6), (16, 8), (32, 4), (32, 6), (32, 8), (64, 4), (64, 6)])
 def test_fp8_decode_compiled_variants(hq, ns):
     rc, why = A.decode_supported((64, hq, 128), C2_CACHE, 256, 4096, dict(num_splits=0, num_stages=ns, TILE_N=16),
                                  kv_dtype="fp8_e4m3")
@@ -125,7 +125,7 @@ def test_fp8_decode_rejections():
     rc, why = A.decode_supported(C2_Q, C2_CACHE, 256, 4096, dict(num_splits=0, num_stages=4, TILE_N=128),
                                  kv_dtype="fp8_e4m3")
     assert rc == _native.UNSUPPORTED_CONFIG and "fp8" in why
-    rc, why = A.decode_supported(C2_Q, C2_CACHE, 256, 4096, dict(num_splits=0, num_stages=6, TILE_N=16),
+    rc, why = A.decode_supported(C2_Q, C2_CACHE, 256, 4096, dict(num_splits=0, num_stages=5, TILE_N=16),
                                  kv_dtype="fp8_e4m3")
     assert rc in (_native.UNSUPPORTED_CONFIG, _native.SMEM_OVERFLOW) and why
 
