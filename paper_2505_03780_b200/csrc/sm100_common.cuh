@@ -150,16 +150,7 @@ __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// kind::f8f6f4 (e4m3 x e4m3 -> f32): D[tmem] (+)= A[smem] * B[smem]^T, K = 32 per instruction.
-__device__ __forceinline__ void umma_f8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                           uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
+// kind::f8f6f4 (e4m3 x e4m3 -> f32): D[tmem] (+)= A[smem] * B[smem]^T, K = 32 bytes per instruction.
 // Warp-convergent, K = 128 as 4 x K32 steps; A advances AS and B advances BS 16-byte units per step.
 template <int AS, int BS>
 __device__ __forceinline__ void umma_f8_ss_k128(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -481,46 +472,6 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
-// kind::f16 instruction descriptor with fp16 A/B (a_format = b_format = 0), fp32 accumulate.
-__host__ __device__ constexpr uint32_t idesc_f16_f32(uint32_t M, uint32_t N, bool a_mn, bool b_mn) {
-  return (1u << 4) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
-}
-
-// Four OCP e4m3 bytes -> four fp16 values scaled by 2^-8, exactly (no rounding, no NaN/Inf out).
-// PRMT with the sign-replicate selector bit spreads byte i into a sign-extended 16-bit lane
-// (b, s) ; << 7 puts the 7 magnitude bits (eeee mmm) into fp16 bits 13..7 and the sign into
-// bit 15; the mask drops the replicated sign at bit 14 and the bits carried in from the lower
-// lane.  An e4m3 exponent e lands in the low 4 bits of the fp16 exponent (bias 15 vs 7), so
-// every value — subnormals included — comes out as x * 2^-8; callers fold 2^8 into the scales.
-__device__ __forceinline__ void e4m3x4_to_f16x4_s8(uint32_t w, uint32_t& lo, uint32_t& hi) {
-  uint32_t a, b;
-  asm("prmt.b32 %0, %1, 0, 0x9180;" : "=r"(a) : "r"(w));
-  asm("prmt.b32 %0, %1, 0, 0xB3A2;" : "=r"(b) : "r"(w));
-  lo = (a << 7) & 0xBF80BF80u;
-  hi = (b << 7) & 0xBF80BF80u;
-}
-
-// Same with the hardware converter (exact, unscaled): two cvt.rn.f16x2.e4m3x2.
-__device__ __forceinline__ void e4m3x4_to_f16x4_hw(uint32_t w, uint32_t& lo, uint32_t& hi) {
-  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
-      "cvt.rn.f16x2.e4m3x2 %0, l;\n\tcvt.rn.f16x2.e4m3x2 %1, h;\n\t}"
-      : "=r"(lo), "=r"(hi)
-      : "r"(w));
-}
-
-// bf16 pair -> fp16 pair (round to nearest); used to retype Q for the fp16 MMA of the fp8 path.
-__device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t w) {
-  uint32_t r;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(w & 0xFFFF0000u)), "f"(__uint_as_float(w << 16)));
-  return r;
-}
-
-__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
-  uint4 v;
-  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-  return v;
-}
-
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");
