@@ -110,6 +110,16 @@ size_t prefill_ws_ints(const b200attn_prefill_params* p, int* nkeys_out) {
   return 3 + (size_t)nkeys + pairs;
 }
 
+// Single-pass speculative softmax on interior tiles (default); B200ATTN_PREFILL_SPECULATE=0 -> two-pass
+bool prefill_speculate() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("B200ATTN_PREFILL_SPECULATE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int NQ, int BN, int NS>
 int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   using C = b200::PrefillCfg<NQ, BN, NS>;
@@ -164,6 +174,7 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   a.single_nqb = single ? (p->max_seqlen + C::BM - 1) / C::BM : 0;
   const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / sqrtf((float)p->head_dim);
   a.scale_log2 = scale * 1.4426950408889634f;
+  a.speculate = prefill_speculate() ? 1 : 0;
   // persistent: never more CTAs than work items (upper bound without a device read)
   const long long items_ub = ((long long)p->total_tokens / 128 + p->num_seqs) * a.num_hg;
   const int ctas = (int)std::min<long long>(num_sms(), std::max<long long>(1, items_ub));

@@ -44,6 +44,7 @@ struct PrefillKernelArgs {
   int32_t single_nqb;  // > 0: one sequence with this many q blocks -> no schedule kernel, items are
                        // q blocks longest first; the work counter is then reset by the last CTA
   float scale_log2;  // softmax_scale * log2(e)
+  int32_t speculate;  // 1: interior tiles take the single-pass path against the running max
 };
 
 template <int NQ, int BN, int NSTAGE_CFG>
@@ -199,6 +200,50 @@ __device__ __forceinline__ float softmax_rowmax(uint32_t s_addr, int kv0, int li
     }
   }
   return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
+}
+
+// Interior tile with a finite running max: exponentials against m_run in ONE pass over S, no max
+// at all.  P is bf16 and O, l are fp32, so a stale max only has to keep 2^(s - m_run) finite: P
+// stays in registers and is stored unless a row sum passed 2^64 (then, rarely, the caller redoes
+// the tile with the exact two-pass path, S still intact in TMEM).  Saves the max pass (a second
+// TMEM read, its load latency and 0.5 FMNMX per score) on nearly every tile.
+template <int BN, int EMU>
+__device__ __forceinline__ bool softmax_speculative(uint32_t s_addr, float sl2, float m_run, float& lsum) {
+  float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  uint32_t pk[BN / 2];
+  const float nmu = -m_run;
+#pragma unroll
+  for (int c = 0; c < BN / 64; ++c) {
+    uint32_t ra[32], rb[32];
+    tmem_ld32x2(s_addr + c * 64, s_addr + c * 64 + 32, ra, rb);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const uint32_t* r = half ? rb : ra;
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        const int k = (i >> 1) & 3;
+        float x0, x1;
+        ffma2(x0, x1, __uint_as_float(r[i]), __uint_as_float(r[i + 1]), sl2, nmu);
+        float e0, e1;
+        if (EMU > 0 && (i >> 1) % EMU == EMU - 1) {
+          exp2_poly2(x0, x1, e0, e1);
+        } else {
+          e0 = fast_exp2(x0);
+          e1 = fast_exp2(x1);
+        }
+        fadd2(ls[2 * k], ls[2 * k + 1], e0, e1);
+        pk[(c * 64 + half * 32 + i) >> 1] = pack_bf16x2(e0, e1);
+      }
+    }
+  }
+  fadd2(ls[0], ls[1], ls[2], ls[3]);
+  fadd2(ls[4], ls[5], ls[6], ls[7]);
+  fadd2(ls[0], ls[1], ls[4], ls[5]);
+  lsum = ls[0] + ls[1];
+  if (!__all_sync(0xffffffffu, m_run != -INFINITY && lsum <= 1.8446744e19f)) return false;  // 2^64
+#pragma unroll
+  for (int g = 0; g < BN / 32; ++g) tmem_st16(s_addr + g * 16, *reinterpret_cast<const uint32_t(*)[16]>(pk + g * 16));
+  return true;
 }
 
 #ifdef B200_TRACE
@@ -436,6 +481,15 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
         // masking is only needed on the diagonal / last tile: decide per warp, keep the common
         // path free of per-element compares and selects
         const bool warp_edge = __any_sync(0xffffffffu, edge);
+        float lsum_spec;
+        if (args.speculate && j > 0 && !warp_edge && softmax_speculative<BN, EMU>(s_addr, sl2, m_run, lsum_spec)) {
+          l_run += lsum_spec;
+          tmem_wait_st();
+          tc_fence_before();
+          if (row == 0) TRACE(2 + t, gt + j);
+          mbar_arrive(&p_full[t]);
+          continue;
+        }
         const float mt = warp_edge ? softmax_rowmax<BN, true>(s_addr, kv0, lim)
                                    : softmax_rowmax<BN, false>(s_addr, kv0, lim);
         const float m_new = fmaxf(m_run, mt * sl2);

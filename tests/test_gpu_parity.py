@@ -163,6 +163,28 @@ def test_prefill_causal(lens):
     check(f"prefill {lens}", out, ref, base)
 
 
+@pytest.mark.parametrize("boost", [6.0, 40.0])
+def test_prefill_score_jumps_after_first_tile(boost):
+    """Keys past the first 2 KV tiles are scaled up so later tiles' scores exceed the running max
+    from the first tile by ~20 (boost 6: the speculative single pass keeps P = 2^(s - m_run) up to
+    2^20 in bf16) or by > 64 (boost 40: the row sum passes 2^64 and the tile is redone exactly)."""
+    g = torch.Generator().manual_seed(7)
+    lens = [1000, 640]
+    T, Hq, Hkv = sum(lens), 16, 4
+    q = torch.randn(T, Hq, 128, generator=g).bfloat16()
+    k = torch.randn(T, Hkv, 128, generator=g)
+    k[256:1000] *= boost
+    k[1000 + 256:] *= boost
+    k = k.bfloat16()
+    v = torch.randn(T, Hkv, 128, generator=g).bfloat16()
+    cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32)
+    ref = oracle.prefill(q, k, v, cu)
+    qd, kd, vd = q.to(DEV), k.to(DEV), v.to(DEV)
+    out = A.prefill_varlen(qd, kd, vd, cu.to(DEV), max(lens), config=pcfg())
+    assert not torch.isnan(out).any()
+    check(f"prefill score jumps x{boost}", out, ref, sdpa_prefill_bf16(qd, kd, vd, cu, True))
+
+
 def test_prefill_noncausal():
     out, ref, base = run_prefill([200, 64, 129], causal=False)
     check("prefill noncausal", out, ref, base)
