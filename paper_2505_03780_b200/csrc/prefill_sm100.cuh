@@ -91,9 +91,16 @@ __device__ __forceinline__ float exp2_poly(float x) {
 
 // Pair version on FFMA2/FADD2: ~5 issue slots per element instead of one MUFU.EX2 (8 MUFU-pipe
 // cycles per warp instruction), so a fraction of the exponentials can move off the MUFU pipe.
+// HI_CLAMP (speculative pass, x may be > 0): clamp at 126 so a huge x gives a huge finite value
+// (like MUFU's inf, it trips the row-sum check) instead of wrapping the exponent field.
+template <bool HI_CLAMP = false>
 __device__ __forceinline__ void exp2_poly2(float x0, float x1, float& y0, float& y1) {
   x0 = fmaxf(x0, -126.0f);
   x1 = fmaxf(x1, -126.0f);
+  if constexpr (HI_CLAMP) {
+    x0 = fminf(x0, 126.0f);
+    x1 = fminf(x1, 126.0f);
+  }
   const float shifter = 12582912.0f;
   float t0, t1, n0, n1;
   ffma2(t0, t1, x0, x1, 1.0f, shifter);
@@ -226,7 +233,7 @@ __device__ __forceinline__ bool softmax_speculative(uint32_t s_addr, float sl2, 
         ffma2(x0, x1, __uint_as_float(r[i]), __uint_as_float(r[i + 1]), sl2, nmu);
         float e0, e1;
         if (EMU > 0 && (i >> 1) % EMU == EMU - 1) {
-          exp2_poly2(x0, x1, e0, e1);
+          exp2_poly2<true>(x0, x1, e0, e1);
         } else {
           e0 = fast_exp2(x0);
           e1 = fast_exp2(x1);
