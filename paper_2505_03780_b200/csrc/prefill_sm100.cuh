@@ -66,12 +66,17 @@ struct PrefillCfg {
   static constexpr int OFF_KV = OFF_Q + QBUF * NQ * Q_BYTES;
   static constexpr int OFF_ITEM = OFF_KV + NSLOT * KV_BYTES;  // int32[2] work-item mailbox
   static constexpr int OFF_BAR = OFF_ITEM + 16;
-  // q_full[2], q_empty[2], kv_full/empty[NSLOT], s_full[NQ], p_full[NQ], o_full, o_free[NQ], item_full/empty[2]
-  static constexpr int NUM_BARS = 4 + 2 * NSLOT + 3 * NQ + 1 + 4;
+  // S_t is double-buffered when TMEM has room (NQ = 2 with BLOCK_N = 64, or NQ = 1): QK_t then runs
+  // two KV steps ahead of PV_t, so the softmax of step j+1 never waits for PV_t(j) + QK_t(j+1)
+  static constexpr int SB = (NQ * 2 * BN + NQ * 128 <= 512) ? 2 : 1;  // S buffers per tile
+  static constexpr int LA = SB;                                       // QK lookahead (KV steps)
+  // q_full[2], q_empty[2], kv_full/empty[NSLOT], s_full[NQ][SB], p_full[NQ][2], o_done[NQ][2],
+  // o_free[NQ], item_full/empty[2]
+  static constexpr int NUM_BARS = 4 + 2 * NSLOT + NQ * SB + 2 * NQ + 2 * NQ + NQ + 4;
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
   static constexpr uint32_t TMEM_COLS = 512;
-  __host__ __device__ static constexpr uint32_t S_COL(int t) { return t * 128; }
-  __host__ __device__ static constexpr uint32_t O_COL(int t) { return 256 + t * 128; }
+  __host__ __device__ static constexpr uint32_t S_COL(int t, int b) { return (t * SB + b) * BN; }
+  __host__ __device__ static constexpr uint32_t O_COL(int t) { return NQ * SB * BN + t * 128; }
   static_assert(BN == 64 || BN == 128, "BLOCK_N in {64,128}");
 };
 
@@ -255,7 +260,7 @@ __device__ __forceinline__ bool softmax_speculative(uint32_t s_addr, float sl2, 
 
 #ifdef B200_TRACE
 // debug-only event trace of CTA 0: [event][slot] clock64 stamps
-__device__ unsigned long long g_trace[8][512];
+__device__ unsigned long long g_trace[16][512];  // 8..11: P done by warp 0..3 of tile 0; 12..15: S seen
 #define TRACE(ev, slot)                                                        \
   do {                                                                        \
     if (blockIdx.x == 0 && (slot) < 512) g_trace[ev][slot] = clock64();        \
@@ -283,11 +288,13 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
   uint64_t* q_empty = bars + 2;  // [2]
   uint64_t* kv_full = bars + 4;
   uint64_t* kv_empty = kv_full + NS;
-  uint64_t* s_full = kv_empty + NS;   // [NQ]
-  uint64_t* p_full = s_full + NQ;     // [NQ]
-  uint64_t* o_full = p_full + NQ;     // [1]
-  uint64_t* o_free = o_full + 1;      // [NQ]
-  uint64_t* item_full = o_free + NQ;  // [2]
+  uint64_t* s_full = kv_empty + NS;       // [NQ][SB]  QK_t landed in S buffer b
+  uint64_t* p_full = s_full + NQ * C::SB;  // [NQ][2]   P_t of a step of that parity written (128 arrivals;
+                                           //           per parity: with the QK lookahead the softmax
+                                           //           may finish step j+1 before the MMA waited step j)
+  uint64_t* o_done = p_full + 2 * NQ;      // [NQ][2]   PV_t of a step of that parity landed
+  uint64_t* o_free = o_done + 2 * NQ;      // [NQ]      epilogue of O_t done (128 arrivals)
+  uint64_t* item_full = o_free + NQ;       // [2]
   uint64_t* item_empty = item_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS);
 
@@ -304,11 +311,13 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
       mbar_init(&kv_empty[i], 1);
     }
     for (int t = 0; t < NQ; ++t) {
-      mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 128);
+      for (int b = 0; b < C::SB; ++b) mbar_init(&s_full[t * C::SB + b], 1);
+      mbar_init(&p_full[2 * t], 128);
+      mbar_init(&p_full[2 * t + 1], 128);
+      mbar_init(&o_done[2 * t], 1);
+      mbar_init(&o_done[2 * t + 1], 1);
       mbar_init(&o_free[t], 128);
     }
-    mbar_init(o_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&item_full[i], 1);
       mbar_init(&item_empty[i], 1 + 128 * NQ);
@@ -379,24 +388,26 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
       const uint64_t q_desc = sdesc_sw128(smem_u32(sQ), 16, 1024);
       const uint64_t k_desc = sdesc_sw128(smem_u32(sKV), 16, 1024);
       const uint64_t v_desc = sdesc_sw128(smem_u32(sKV), C::HALF_KV, 1024);
+      constexpr int SB = C::SB, LA = C::LA;
       int qb = 0;
-      auto issue_qk = [&](int t, int slot) {
+      auto issue_qk = [&](int t, int slot, int buf) {
         const uint64_t qa = q_desc + (((qb * NQ + t) * C::Q_BYTES) >> 4);
         const uint64_t kb = k_desc + ((slot * C::KV_BYTES) >> 4);
-        umma_ss_k128<2, C::HALF_Q / 16, 2, C::HALF_KV / 16>(tmem + C::S_COL(t), qa, kb, IDESC_QK, 0u);
+        umma_ss_k128<2, C::HALF_Q / 16, 2, C::HALF_KV / 16>(tmem + C::S_COL(t, buf), qa, kb, IDESC_QK, 0u);
       };
-      auto issue_pv = [&](int t, int slot, bool acc) {
+      auto issue_pv = [&](int t, int slot, int buf, bool acc) {
         const uint64_t vb = v_desc + ((slot * C::KV_BYTES) >> 4);
         if constexpr (BN == 128) {
-          umma_ts_k128<128, 512>(tmem + C::O_COL(t), tmem + C::S_COL(t), vb, IDESC_PV, acc ? 1u : 0u);
+          umma_ts_k128<128, 512>(tmem + C::O_COL(t), tmem + C::S_COL(t, buf), vb, IDESC_PV, acc ? 1u : 0u);
         } else {
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
-            umma_ts_w(tmem + C::O_COL(t), tmem + C::S_COL(t) + kk * 8, vb + ((kk * 16 * 128) >> 4), IDESC_PV,
+            umma_ts_w(tmem + C::O_COL(t), tmem + C::S_COL(t, buf) + kk * 8, vb + ((kk * 16 * 128) >> 4), IDESC_PV,
                       (acc || kk > 0) ? 1u : 0u);
         }
       };
-      int ri = 0, gt = 0;
+      // ring positions follow the TMA's load order: K_s at rbase + 2s, V_s at rbase + 2s + 1
+      int rbase = 0, gt = 0;
       for (int k = 0;; ++k) {
         mbar_wait(&item_full[k & 1], (k >> 1) & 1);
         const int w = item_box[k & 1];
@@ -409,49 +420,42 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
         const int n_kv = n_kv_of(args.cu_seqlens[seq + 1] - seq_start, qblk);
         qb = (C::QBUF == 2) ? (k & 1) : 0;
         mbar_wait(&q_full[qb], (C::QBUF == 2) ? ((k >> 1) & 1) : (k & 1));
-        {
-          const int slot = ri % NS;
-          mbar_wait(&kv_full[slot], (ri / NS) & 1);
-          tc_fence_after();
-          for (int t = 0; t < NQ; ++t) {
-            issue_qk(t, slot);
-            umma_commit_w(&s_full[t]);
+        // QK_t(s) of step s for tile t; per tile, step s uses S buffer (gt + s) % SB
+        auto qk_step_tile = [&](int s, int t) {
+          const int ki = rbase + 2 * s, kslot = ki % NS;
+          if (t == 0) {
+            mbar_wait(&kv_full[kslot], (ki / NS) & 1);
+            tc_fence_after();
           }
-          umma_commit_w(&kv_empty[slot]);
-          if (n_kv == 1) umma_commit_w(&q_empty[qb]);
-          ++ri;
-        }
+          const int buf = (gt + s) % SB;
+          issue_qk(t, kslot, buf);
+          umma_commit_w(&s_full[t * SB + buf]);
+          if (t == NQ - 1) {
+            umma_commit_w(&kv_empty[kslot]);
+            if (s == n_kv - 1) umma_commit_w(&q_empty[qb]);
+          }
+        };
+        for (int s = 0; s < LA && s < n_kv; ++s)
+          for (int t = 0; t < NQ; ++t) qk_step_tile(s, t);
         for (int j = 0; j < n_kv; ++j) {
-          const int vslot = ri % NS;
-          mbar_wait(&kv_full[vslot], (ri / NS) & 1);
+          const int vi = rbase + 2 * j + 1, vslot = vi % NS;
+          mbar_wait(&kv_full[vslot], (vi / NS) & 1);
           TRACE(6, gt + j);
-          ++ri;
-          const bool more = (j + 1) < n_kv;
-          const int kslot = ri % NS;
           for (int t = 0; t < NQ; ++t) {
-            mbar_wait(&p_full[t], (gt + j) & 1);
+            mbar_wait(&p_full[2 * t + ((gt + j) & 1)], ((gt + j) >> 1) & 1);
             TRACE(4 + t, gt + j);
             if (j == 0 && k > 0) mbar_wait(&o_free[t], (k - 1) & 1);
             tc_fence_after();
-            issue_pv(t, vslot, j > 0);
+            issue_pv(t, vslot, (gt + j) % SB, j > 0);
+            umma_commit_w(&o_done[2 * t + ((gt + j) & 1)]);
             if (t == NQ - 1) umma_commit_w(&kv_empty[vslot]);
-            if (more) {
-              if (t == 0) {
-                mbar_wait(&kv_full[kslot], (ri / NS) & 1);
-                tc_fence_after();
-              }
-              issue_qk(t, kslot);
+            if (j + LA < n_kv) {
+              qk_step_tile(j + LA, t);
               if (t == 0) TRACE(7, gt + j);
-              umma_commit_w(&s_full[t]);
-              if (t == NQ - 1) {
-                umma_commit_w(&kv_empty[kslot]);
-                if (j + 2 == n_kv) umma_commit_w(&q_empty[qb]);
-              }
             }
           }
-          if (more) ++ri;
         }
-        umma_commit_w(o_full);
+        rbase += 2 * n_kv;
         gt += n_kv;
       }
     }
@@ -460,7 +464,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
     const int t = warp >> 2;
     const int row = ((warp & 3) << 5) + lane;  // query row within the block == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) << 5) << 16;
-    const uint32_t s_addr = tmem + lane_base + C::S_COL(t);
+    const uint32_t s_base = tmem + lane_base;
     const uint32_t o_addr = tmem + lane_base + C::O_COL(t);
     const float sl2 = args.scale_log2;
     int gt = 0;
@@ -480,9 +484,12 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
       float m_run = -INFINITY, l_run = 0.f;
 
       for (int j = 0; j < n_kv; ++j) {
-        mbar_wait(&s_full[t], (gt + j) & 1);
+        const int buf = (gt + j) % C::SB;
+        mbar_wait(&s_full[t * C::SB + buf], ((gt + j) / C::SB) & 1);
         tc_fence_after();
+        const uint32_t s_addr = s_base + C::S_COL(t, buf);
         if (row == 0) TRACE(t, gt + j);
+        if (t == 0 && lane == 0) TRACE(12 + warp, gt + j);
         const int kv0 = j * BN;
         const bool edge = (kv0 + BN > kv_end) || (args.causal && kv0 + BN - 1 > q_pos);
         // masking is only needed on the diagonal / last tile: decide per warp, keep the common
@@ -494,7 +501,8 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
           tmem_wait_st();
           tc_fence_before();
           if (row == 0) TRACE(2 + t, gt + j);
-          mbar_arrive(&p_full[t]);
+          if (t == 0 && lane == 0) TRACE(8 + warp, gt + j);
+          mbar_arrive(&p_full[2 * t + ((gt + j) & 1)]);
           continue;
         }
         const float mt = warp_edge ? softmax_rowmax<BN, true>(s_addr, kv0, lim)
@@ -508,6 +516,11 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
           l_run *= alpha;
         }
         if (j > 0 && __any_sync(0xffffffffu, need && alpha != 1.f)) {
+          // O_t must hold PV_t(j-1) before it is rescaled (with the QK lookahead it may still be
+          // in flight); per-parity barriers keep the phase unambiguous (PV_t(j-3) has landed and
+          // PV_t(j+1) cannot be issued yet)
+          mbar_wait(&o_done[2 * t + ((gt + j - 1) & 1)], ((gt + j - 1) >> 1) & 1);
+          tc_fence_after();
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t r[32];
@@ -524,11 +537,12 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
         tmem_wait_st();
         tc_fence_before();
         if (row == 0) TRACE(2 + t, gt + j);
-        mbar_arrive(&p_full[t]);
+        if (t == 0 && lane == 0) TRACE(8 + warp, gt + j);
+        mbar_arrive(&p_full[2 * t + ((gt + j) & 1)]);
       }
 
       // ---------------------------------------------------------- epilogue for this item
-      mbar_wait(o_full, k & 1);
+      mbar_wait(&o_done[2 * t + ((gt + n_kv - 1) & 1)], ((gt + n_kv - 1) >> 1) & 1);  // last PV_t
       tc_fence_after();
       const int h = hg * NQ + t;
       const bool valid = q_pos < seq_len;
