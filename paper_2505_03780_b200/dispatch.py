@@ -73,9 +73,23 @@ def table() -> dict:
 def reset():
     global _table
     _table = None
+    _lookup_cache.clear()
+
+
+_lookup_cache: dict = {}
 
 
 def lookup(op: str, dims: dict) -> Optional[dict]:
+    """Nearest tuned config (memoised per (op, dims): a serving loop asks the same shape every step)."""
+    key = (op, tuple(sorted(dims.items())))
+    if key in _lookup_cache:
+        return _lookup_cache[key]
+    cfg = _lookup(op, dims)
+    _lookup_cache[key] = cfg
+    return cfg
+
+
+def _lookup(op: str, dims: dict) -> Optional[dict]:
     rows = table().get(op, [])
     best, best_d = None, math.inf
     for shape, cfg in rows:
