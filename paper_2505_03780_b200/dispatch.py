@@ -101,16 +101,32 @@ def _lookup(op: str, dims: dict) -> Optional[dict]:
         for k in ("batch_size", "seq_len"):
             if k in shape and k in dims and shape[k] and dims[k]:
                 d += abs(math.log2(float(shape[k])) - math.log2(float(dims[k])))
+        # prefill: varlen batches differ from uniform ones of the same (batch, max length) in their
+        # token count; tuned varlen rows (e.g. C3) carry it, uniform rows imply batch * seq_len
+        if op == "prefill" and dims.get("total_tokens"):
+            tok = _row_tokens(shape)
+            if tok:
+                d += abs(math.log2(float(tok)) - math.log2(float(dims["total_tokens"])))
         if d < best_d:
             best, best_d = cfg, d
     return best
+
+
+def _row_tokens(shape: dict) -> int:
+    if "seq_len" in shape and "batch_size" in shape:
+        return int(shape["batch_size"]) * int(shape["seq_len"])
+    if "seq_len_min" in shape:
+        from .workload import varlen_lengths
+
+        return sum(varlen_lengths(shape))
+    return 0
 
 
 def default_prefill_config(**dims) -> dict:
     dims = dict(dims)
     num_seqs = dims.pop("num_seqs", 1)
     dims["batch_size"] = num_seqs
-    dims["seq_len"] = dims.get("max_seqlen", 0)
+    dims["seq_len"] = dims.get("max_seqlen", 0) or dims.get("seq_len_max", 0)
     cfg = lookup("prefill", dims)
     if cfg is None:
         cfg = PREFILL_DEFAULT

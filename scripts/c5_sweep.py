@@ -41,6 +41,16 @@ SPACE = {"prefill": "flash_attention.space.json", "decode": "paged_decode.space.
 BINDING = {"prefill": "prefill.binding.json", "decode": "decode.binding.json"}
 
 
+# BASELINE.json shapes off the batch x seq grid: C3 (varlen, geometric 128..8192) and one GPU's
+# shard of C4 (64 q heads, 32 x 32k) — the configs the bench reports get their own tuned rows
+EXTRA = {
+    "prefill": [{"op": "prefill", "batch_size": 16, "seq_len_min": 128, "seq_len_max": 8192, "len_dist": "geometric",
+                 **HEADS, "causal": True, "dtype": "bfloat16", "seed": 0}],
+    "decode": [{"op": "decode", "batch_size": 32, "seq_len": 32768, "num_q_heads": 64, "num_kv_heads": 8,
+                "head_dim": 128, "block_size": 16, "dtype": "bfloat16", "seed": 0}],
+}
+
+
 def shapes_for(op: str, quick: bool) -> list[dict]:
     bs = [1, 4, 16, 64] if quick else BATCHES
     ss = [512, 2048, 8192] if quick else SEQS
@@ -69,7 +79,7 @@ def cmd_run(a):
     out = Path(a.out)
     out.mkdir(parents=True, exist_ok=True)
     for op in a.ops.split(","):
-        shapes = shapes_for(op, a.quick)
+        shapes = EXTRA[op] if a.extra_only else shapes_for(op, a.quick) + EXTRA[op]
         sf = out / f"{op}_shapes.json"
         sf.write_text(json.dumps(shapes, indent=1))
         runner = f"{sys.executable} -m paper_2505_03780_b200.runner --binding {SPACES / BINDING[op]} --protocol 1 --backend {a.backend}"
@@ -129,7 +139,8 @@ def cmd_post(a):
             dims = {k: v for k, v in shape.items()}
             if op == "prefill":
                 hcfg = dispatch.PREFILL_DEFAULT
-                items_paired = dims["batch_size"] * ((dims["seq_len"] + 127) // 128) * dims["num_q_heads"] // 2
+                items_paired = dims["batch_size"] * ((dims.get("seq_len", dims.get("seq_len_max", 0)) + 127) // 128) * \
+                    dims["num_q_heads"] // 2
                 if items_paired < 148:
                     hcfg = dict(hcfg, BLOCK_M=128)
             else:
@@ -151,13 +162,13 @@ def cmd_post(a):
             p = out / f"{op}_{name}.csv"
             if not rows:
                 return None
-            cols = sorted(rows[0][0].keys())
+            cols = sorted({c for d, _ in rows for c in d.keys()})
             with open(p, "w", newline="") as fh:
                 w = csv.writer(fh)
                 w.writerow(["impl", *cols, "median_ms"])
                 for dims, ms in rows:
-                    w.writerow([impl, *[json.dumps(dims[c]) if isinstance(dims[c], bool) else dims[c] for c in cols],
-                                repr(ms)])
+                    w.writerow([impl, *[json.dumps(dims[c]) if isinstance(dims.get(c), bool) else dims.get(c, "")
+                                        for c in cols], repr(ms)])
             return p
 
         t_csv = write_csv("tuned", "tuned", [(d, m) for d, m in ((r["shape"], r["median_ms"]) for r in per_shape
@@ -185,8 +196,13 @@ def cmd_post(a):
         md += [f"## {op}", "", "| batch | seq | best | tuned ms | fixed ms | speed-up vs fixed | heuristic ms |",
                "|---|---|---|---|---|---|---|"]
         for r in sorted((r for r in per_shape if r.get("best")),
-                        key=lambda r: (r["shape"]["batch_size"], r["shape"]["seq_len"])):
-            s = r["shape"]
+                        key=lambda r: (r["shape"]["batch_size"], r["shape"].get("seq_len", 0),
+                                       r["shape"]["num_q_heads"])):
+            s = dict(r["shape"])
+            if "seq_len" not in s:
+                s["seq_len"] = f"{s['seq_len_min']}..{s['seq_len_max']}"
+            if s["num_q_heads"] != 32:
+                s["seq_len"] = f"{s['seq_len']} ({s['num_q_heads']}q)"
             bst = ",".join(f"{k}={v}" for k, v in sorted(r["best"].items()))
             fx = r.get("fixed_ms")
             md.append(f"| {s['batch_size']} | {s['seq_len']} | {bst} | {r['median_ms']:.4f} | "
@@ -214,6 +230,7 @@ def main():
     ap.add_argument("--out", default="gpurun_out/c5")
     ap.add_argument("--ops", default="prefill,decode")
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--extra-only", action="store_true", help="only the BASELINE shapes off the grid (C3, C4 shard)")
     ap.add_argument("--timeout-ms", type=float, default=300000.0)
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--backend", default="b200", help="stub: protocol/post-processing dry run without a GPU")
