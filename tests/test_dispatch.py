@@ -1,0 +1,63 @@
+"""Per-shape dispatch table: lookups against the shipped table and synthetic ones."""
+import json
+
+import pytest
+
+from paper_2505_03780_b200 import dispatch as D
+
+HEADS = dict(num_q_heads=32, num_kv_heads=8, head_dim=128)
+
+
+@pytest.fixture()
+def table(tmp_path, monkeypatch):
+    rows = [
+        {"shape": dict(op="prefill", batch_size=16, seq_len=8192, causal=True, **HEADS),
+         "best": dict(BLOCK_M=256, BLOCK_N=128, num_warps=4, num_stages=4, waves_per_eu=1, PRE_LOAD_V=False)},
+        {"shape": dict(op="prefill", batch_size=16, seq_len_min=128, seq_len_max=8192, len_dist="geometric",
+                       causal=True, **HEADS),
+         "best": dict(BLOCK_M=128, BLOCK_N=128, num_warps=4, num_stages=3, waves_per_eu=1, PRE_LOAD_V=False)},
+        {"shape": dict(op="decode", batch_size=64, seq_len=4096, block_size=16, **HEADS),
+         "best": dict(num_splits=0, num_stages=5, TILE_N=16)},
+    ]
+    p = tmp_path / "t.json"
+    p.write_text(json.dumps({"rows": rows}))
+    monkeypatch.setenv("B200ATTN_DISPATCH", str(p))
+    D.reset()
+    yield
+    D.reset()
+
+
+def test_varlen_row_wins_on_token_count(table):
+    c3 = D.default_prefill_config(num_seqs=16, total_tokens=33430, max_seqlen=8192, causal=True, **HEADS)
+    assert c3["BLOCK_M"] == 128 and c3["num_stages"] == 3
+    uniform = D.default_prefill_config(num_seqs=16, total_tokens=16 * 8192, max_seqlen=8192, causal=True, **HEADS)
+    assert uniform["BLOCK_M"] == 256 and uniform["num_stages"] == 4
+
+
+def test_kv_dtype_is_part_of_the_geometry(table):
+    bf16 = D.default_decode_config(batch_size=64, seq_len=4096, block_size=16, **HEADS)
+    assert bf16 == {"num_splits": 0, "num_stages": 5, "TILE_N": 16}
+    fp8 = D.default_decode_config(batch_size=64, seq_len=4096, block_size=16, kv_dtype="fp8_e4m3", **HEADS)
+    assert fp8["TILE_N"] == 16 and fp8["num_stages"] == D.FP8_DECODE_STAGES[4]
+
+
+def test_lookup_is_memoised_and_returns_copies(table):
+    a = D.default_decode_config(batch_size=64, seq_len=4096, block_size=16, **HEADS)
+    a["num_stages"] = 99
+    b = D.default_decode_config(batch_size=64, seq_len=4096, block_size=16, **HEADS)
+    assert b["num_stages"] == 5
+    assert len(D._lookup_cache) >= 1
+
+
+def test_odd_gqa_group_never_pairs_heads(table):
+    c = D.default_prefill_config(num_seqs=16, total_tokens=131072, max_seqlen=8192, causal=True, num_q_heads=24,
+                                 num_kv_heads=8, head_dim=128)
+    assert c["BLOCK_M"] == 128
+
+
+def test_shipped_table_covers_the_baseline_configs():
+    D.reset()
+    rows = D.table()
+    assert len(rows["prefill"]) >= 78 and len(rows["decode"]) >= 81
+    c2 = D.default_decode_config(batch_size=64, seq_len=4096, block_size=16, **HEADS)
+    assert c2["TILE_N"] == 16
