@@ -101,7 +101,10 @@ int num_sms();
 
 // ------------------------------------------------------------------ prefill variants
 using PrefillLauncher = int (*)(const b200attn_prefill_params*, cudaStream_t);
-constexpr int kPrefillEmu = 3;  // 1 pair in 3 on the FMA pipe (C3: EMU 0: 987, 3: 1008, 4: 1003, 6: 1004 TFLOP/s)
+#ifndef B200_PREFILL_EMU
+#define B200_PREFILL_EMU 3
+#endif
+constexpr int kPrefillEmu = B200_PREFILL_EMU;  // 1 pair in 3 on the FMA pipe (C3: EMU 0: 987, 3: 1008, 4: 1003, 6: 1004 TFLOP/s)
 
 size_t prefill_ws_ints(const b200attn_prefill_params* p, int* nkeys_out) {
   const int nkeys = (p->max_seqlen + 127) / 128;

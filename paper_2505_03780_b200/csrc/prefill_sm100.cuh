@@ -141,45 +141,45 @@ __device__ __forceinline__ void prefill_decode_item(int w, const PrefillKernelAr
 // per-element compare/select at all — predicated-off instructions still cost issue slots.
 template <int BN, bool MASKED, int EMU>
 __device__ __forceinline__ float softmax_pass2(uint32_t s_addr, float sl2, float nmu, int kv0, int lim) {
-  // four independent FADD2 accumulators: a single running sum is a 64-deep dependent chain
+  // four independent FADD2 accumulators: a single running sum is a 64-deep dependent chain;
+  // 32-column chunks with the next chunk's tcgen05.ld in flight (P of chunk c lands on S
+  // columns [16c, 16c + 16), all of which were loaded before)
   float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  uint32_t r[2][32];
+  tmem_ld32_nowait(s_addr, r[0]);
+  tmem_wait_ld_regs(r[0]);
 #pragma unroll
-  for (int c = 0; c < BN / 64; ++c) {
-    uint32_t ra[32], rb[32];
-    tmem_ld32x2(s_addr + c * 64, s_addr + c * 64 + 32, ra, rb);
-    uint32_t pa[16], pb[16];
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t(&cur)[32] = r[c & 1];
+    if (c + 1 < BN / 32) tmem_ld32_nowait(s_addr + (c + 1) * 32, r[(c + 1) & 1]);
+    uint32_t pk[16];
+    const int col0 = kv0 + c * 32;
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const uint32_t* r = half ? rb : ra;
-      uint32_t* pk = half ? pb : pa;
-      const int col0 = kv0 + c * 64 + half * 32;
-#pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        float x0, x1;
-        ffma2(x0, x1, __uint_as_float(r[i]), __uint_as_float(r[i + 1]), sl2, nmu);
-        float e0, e1;
-        if constexpr (!MASKED && EMU > 0) {
-          if ((i >> 1) % EMU == EMU - 1) {
-            exp2_poly2(x0, x1, e0, e1);
-          } else {
-            e0 = fast_exp2(x0);
-            e1 = fast_exp2(x1);
-          }
+    for (int i = 0; i < 32; i += 2) {
+      float x0, x1;
+      ffma2(x0, x1, __uint_as_float(cur[i]), __uint_as_float(cur[i + 1]), sl2, nmu);
+      float e0, e1;
+      if constexpr (!MASKED && EMU > 0) {
+        if ((i >> 1) % EMU == EMU - 1) {
+          exp2_poly2(x0, x1, e0, e1);
         } else {
           e0 = fast_exp2(x0);
           e1 = fast_exp2(x1);
         }
-        if constexpr (MASKED) {
-          if (col0 + i > lim) e0 = 0.f;
-          if (col0 + i + 1 > lim) e1 = 0.f;
-        }
-        const int acc = ((i >> 1) & 3) * 2;
-        fadd2(ls[acc], ls[acc + 1], e0, e1);
-        pk[i >> 1] = pack_bf16x2(e0, e1);
+      } else {
+        e0 = fast_exp2(x0);
+        e1 = fast_exp2(x1);
       }
+      if constexpr (MASKED) {
+        if (col0 + i > lim) e0 = 0.f;
+        if (col0 + i + 1 > lim) e1 = 0.f;
+      }
+      const int acc = ((i >> 1) & 3) * 2;
+      fadd2(ls[acc], ls[acc + 1], e0, e1);
+      pk[i >> 1] = pack_bf16x2(e0, e1);
     }
-    tmem_st16(s_addr + c * 32, pa);  // P overwrites S columns this thread has already read
-    tmem_st16(s_addr + c * 32 + 16, pb);
+    if (c + 1 < BN / 32) tmem_wait_ld_regs(r[(c + 1) & 1]);
+    tmem_st16(s_addr + c * 16, pk);  // P overwrites S columns this thread has already read
   }
   fadd2(ls[0], ls[1], ls[2], ls[3]);
   fadd2(ls[4], ls[5], ls[6], ls[7]);
@@ -189,27 +189,27 @@ __device__ __forceinline__ float softmax_pass2(uint32_t s_addr, float sl2, float
 
 template <int BN, bool MASKED>
 __device__ __forceinline__ float softmax_rowmax(uint32_t s_addr, int kv0, int lim) {
-  // four independent 3-input max chains (FMNMX3) instead of one 64-deep chain
+  // four independent 3-input max chains (FMNMX3); all chunk loads in flight before one wait
   float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  uint32_t r[2][32];
+  tmem_ld32_nowait(s_addr, r[0]);
+  tmem_wait_ld_regs(r[0]);
 #pragma unroll
-  for (int c = 0; c < BN / 64; ++c) {
-    uint32_t ra[32], rb[32];
-    tmem_ld32x2(s_addr + c * 64, s_addr + c * 64 + 32, ra, rb);
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t(&cur)[32] = r[c & 1];
+    if (c + 1 < BN / 32) tmem_ld32_nowait(s_addr + (c + 1) * 32, r[(c + 1) & 1]);
 #pragma unroll
     for (int i = 0; i < 32; i += 2) {
-      float a0 = __uint_as_float(ra[i]), a1 = __uint_as_float(ra[i + 1]);
-      float b0 = __uint_as_float(rb[i]), b1 = __uint_as_float(rb[i + 1]);
+      float a0 = __uint_as_float(cur[i]), a1 = __uint_as_float(cur[i + 1]);
       if constexpr (MASKED) {
-        const int ca = kv0 + c * 64 + i, cb = ca + 32;
+        const int ca = kv0 + c * 32 + i;
         if (ca > lim) a0 = -INFINITY;
         if (ca + 1 > lim) a1 = -INFINITY;
-        if (cb > lim) b0 = -INFINITY;
-        if (cb + 1 > lim) b1 = -INFINITY;
       }
-      const int k = (i >> 1) & 1;
+      const int k = (i >> 1) & 3;
       m[k] = fmaxf(m[k], fmaxf(a0, a1));
-      m[2 + k] = fmaxf(m[2 + k], fmaxf(b0, b1));
     }
+    if (c + 1 < BN / 32) tmem_wait_ld_regs(r[(c + 1) & 1]);
   }
   return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
 }
@@ -224,29 +224,31 @@ __device__ __forceinline__ bool softmax_speculative(uint32_t s_addr, float sl2, 
   float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   uint32_t pk[BN / 2];
   const float nmu = -m_run;
+  // 32-column chunks, software-pipelined: chunk c+1's tcgen05.ld is in flight while chunk c is
+  // exponentiated, so the TMEM load latency is paid once per tile instead of once per chunk
+  uint32_t r[2][32];
+  tmem_ld32_nowait(s_addr, r[0]);
+  tmem_wait_ld_regs(r[0]);
 #pragma unroll
-  for (int c = 0; c < BN / 64; ++c) {
-    uint32_t ra[32], rb[32];
-    tmem_ld32x2(s_addr + c * 64, s_addr + c * 64 + 32, ra, rb);
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t(&cur)[32] = r[c & 1];
+    if (c + 1 < BN / 32) tmem_ld32_nowait(s_addr + (c + 1) * 32, r[(c + 1) & 1]);
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const uint32_t* r = half ? rb : ra;
-#pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        const int k = (i >> 1) & 3;
-        float x0, x1;
-        ffma2(x0, x1, __uint_as_float(r[i]), __uint_as_float(r[i + 1]), sl2, nmu);
-        float e0, e1;
-        if (EMU > 0 && (i >> 1) % EMU == EMU - 1) {
-          exp2_poly2<true>(x0, x1, e0, e1);
-        } else {
-          e0 = fast_exp2(x0);
-          e1 = fast_exp2(x1);
-        }
-        fadd2(ls[2 * k], ls[2 * k + 1], e0, e1);
-        pk[(c * 64 + half * 32 + i) >> 1] = pack_bf16x2(e0, e1);
+    for (int i = 0; i < 32; i += 2) {
+      const int k = (i >> 1) & 3;
+      float x0, x1;
+      ffma2(x0, x1, __uint_as_float(cur[i]), __uint_as_float(cur[i + 1]), sl2, nmu);
+      float e0, e1;
+      if (EMU > 0 && (i >> 1) % EMU == EMU - 1) {
+        exp2_poly2<true>(x0, x1, e0, e1);
+      } else {
+        e0 = fast_exp2(x0);
+        e1 = fast_exp2(x1);
       }
+      fadd2(ls[2 * k], ls[2 * k + 1], e0, e1);
+      pk[(c * 32 + i) >> 1] = pack_bf16x2(e0, e1);
     }
+    if (c + 1 < BN / 32) tmem_wait_ld_regs(r[(c + 1) & 1]);
   }
   fadd2(ls[0], ls[1], ls[2], ls[3]);
   fadd2(ls[4], ls[5], ls[6], ls[7]);

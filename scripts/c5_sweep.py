@@ -80,6 +80,8 @@ def cmd_run(a):
     out.mkdir(parents=True, exist_ok=True)
     for op in a.ops.split(","):
         shapes = EXTRA[op] if a.extra_only else shapes_for(op, a.quick) + EXTRA[op]
+        if a.shapes:  # an explicit subset (e.g. the shapes a timed-out run did not reach)
+            shapes = [d for d in json.loads(Path(a.shapes).read_text()) if d["op"] == op]
         sf = out / f"{op}_shapes.json"
         sf.write_text(json.dumps(shapes, indent=1))
         runner = f"{sys.executable} -m paper_2505_03780_b200.runner --binding {SPACES / BINDING[op]} --protocol 1 --backend {a.backend}"
@@ -233,6 +235,7 @@ def main():
     ap.add_argument("--batch", type=int, default=1,
                     help="launches per timed graph replay, reported per launch (1 = the reference's semantics)")
     ap.add_argument("--extra-only", action="store_true", help="only the BASELINE shapes off the grid (C3, C4 shard)")
+    ap.add_argument("--shapes", help="JSON list of shape dicts to sweep instead of the grid")
     ap.add_argument("--timeout-ms", type=float, default=300000.0)
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--backend", default="b200", help="stub: protocol/post-processing dry run without a GPU")
