@@ -86,6 +86,7 @@ class B200Backend:
         self._shape_key = None
         self._inputs = None
         self.batch = max(1, int(os.environ.get("B200ATTN_RUNNER_BATCH", "1")))
+        self.cooldown_s = float(os.environ.get("B200ATTN_RUNNER_COOLDOWN_MS", "0")) / 1000.0
 
     @staticmethod
     def _query_device(idx: int):
@@ -199,6 +200,8 @@ class B200Backend:
             except RuntimeError:
                 nb = 1
                 replay = launch
+            if self.cooldown_s > 0:  # start every config from the same thermal / power state
+                time.sleep(self.cooldown_s)
             for _ in range(warmups):
                 replay()
             torch.cuda.synchronize()

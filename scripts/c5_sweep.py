@@ -66,8 +66,9 @@ def shapes_for(op: str, quick: bool) -> list[dict]:
     return out
 
 
-def ktune(*args, check=True, batch=1):
-    env = dict(os.environ, PYTHONPATH=os.pathsep.join([str(REF), str(ROOT)]), B200ATTN_RUNNER_BATCH=str(batch))
+def ktune(*args, check=True, batch=1, cooldown_ms=0.0):
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([str(REF), str(ROOT)]), B200ATTN_RUNNER_BATCH=str(batch),
+               B200ATTN_RUNNER_COOLDOWN_MS=str(cooldown_ms))
     r = subprocess.run([sys.executable, "-m", "ktune", *args], env=env, capture_output=True, text=True)
     if check and r.returncode != 0:
         sys.stderr.write(r.stdout[-4000:] + r.stderr[-4000:])
@@ -87,7 +88,8 @@ def cmd_run(a):
         runner = f"{sys.executable} -m paper_2505_03780_b200.runner --binding {SPACES / BINDING[op]} --protocol 1 --backend {a.backend}"
         r = ktune("tune", "--space", str(SPACES / SPACE[op]), "--runner", runner, "--shapes", str(sf),
                   "--strategy", "exhaustive", "--cache-dir", str(out / "cache"), "--out", str(out / f"{op}_results"),
-                  "--timeout-ms", str(a.timeout_ms), "--json", check=False, batch=a.batch)
+                  "--timeout-ms", str(a.timeout_ms), "--json", check=False, batch=a.batch,
+                  cooldown_ms=a.cooldown_ms)
         (out / f"{op}_tune.json").write_text(r.stdout)
         (out / f"{op}_tune.err").write_text(r.stderr[-20000:])
         print(f"{op}: ktune tune rc={r.returncode}", flush=True)
@@ -236,6 +238,7 @@ def main():
                     help="launches per timed graph replay, reported per launch (1 = the reference's semantics)")
     ap.add_argument("--extra-only", action="store_true", help="only the BASELINE shapes off the grid (C3, C4 shard)")
     ap.add_argument("--shapes", help="JSON list of shape dicts to sweep instead of the grid")
+    ap.add_argument("--cooldown-ms", type=float, default=0.0, help="idle before timing each config (thermal state)")
     ap.add_argument("--timeout-ms", type=float, default=300000.0)
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--backend", default="b200", help="stub: protocol/post-processing dry run without a GPU")
