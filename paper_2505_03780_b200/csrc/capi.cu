@@ -123,10 +123,10 @@ bool prefill_speculate() {
   return v == 1;
 }
 
-template <int NQ, int BN, int NS>
+template <int NQ, int BN, int NS, int SPLIT>
 int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
-  using C = b200::PrefillCfg<NQ, BN, NS>;
-  auto kern = b200::prefill_fwd_kernel<NQ, BN, NS, kPrefillEmu>;
+  using C = b200::PrefillCfg<NQ, BN, NS, SPLIT>;
+  auto kern = b200::prefill_fwd_kernel<NQ, BN, NS, kPrefillEmu, SPLIT>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -188,16 +188,22 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
 }
 
 struct PrefillEntry {
-  int nq, bn, ns;
+  int nq, bn, ns, nw;
   PrefillLauncher fn;
   int smem;
 };
 
-#define PF(NQ, BN, NS) {NQ, BN, NS, &launch_prefill<NQ, BN, NS>, b200::PrefillCfg<NQ, BN, NS>::SMEM_BYTES}
+// num_warps = softmax warps per 128-row Q tile: 4 (one thread per S row) or 8 (two threads per
+// row, 64 columns each; BLOCK_N = 128 only, and the space's num_warps * num_stages <= 16 caps
+// num_stages at 2)
+#define PF(NQ, BN, NS, NW)                                                 \
+  {NQ, BN, NS, NW, &launch_prefill<NQ, BN, NS, NW / 4>,                    \
+   b200::PrefillCfg<NQ, BN, NS, NW / 4>::SMEM_BYTES}
 const PrefillEntry kPrefill[] = {
-    PF(2, 128, 1), PF(2, 128, 2), PF(2, 128, 3), PF(2, 128, 4), PF(2, 64, 1), PF(2, 64, 2), PF(2, 64, 3),
-    PF(2, 64, 4),  PF(1, 128, 1), PF(1, 128, 2), PF(1, 128, 3), PF(1, 128, 4), PF(1, 64, 1), PF(1, 64, 2),
-    PF(1, 64, 3),  PF(1, 64, 4),
+    PF(2, 128, 1, 4), PF(2, 128, 2, 4), PF(2, 128, 3, 4), PF(2, 128, 4, 4), PF(2, 64, 1, 4),  PF(2, 64, 2, 4),
+    PF(2, 64, 3, 4),  PF(2, 64, 4, 4),  PF(1, 128, 1, 4), PF(1, 128, 2, 4), PF(1, 128, 3, 4), PF(1, 128, 4, 4),
+    PF(1, 64, 1, 4),  PF(1, 64, 2, 4),  PF(1, 64, 3, 4),  PF(1, 64, 4, 4),  PF(2, 128, 1, 8), PF(2, 128, 2, 8),
+    PF(1, 128, 1, 8), PF(1, 128, 2, 8),
 };
 #undef PF
 
@@ -210,10 +216,13 @@ int check_prefill(const b200attn_prefill_params* p, const b200attn_prefill_varia
                 v->block_m);
   if (v->block_n != 64 && v->block_n != 128)
     return fail(B200ATTN_UNSUPPORTED_CONFIG, "BLOCK_N=%d: compiled K/V tiles are 64 or 128 rows", v->block_n);
-  if (v->num_warps != 4)
+  if (v->num_warps != 4 && v->num_warps != 8)
     return fail(B200ATTN_UNSUPPORTED_CONFIG,
-                "num_warps=%d: the softmax warpgroup is 4 warps (one thread per TMEM lane of the 128-row tile)",
+                "num_warps=%d: a 128-row Q tile has 4 softmax warps (one thread per TMEM lane) or 8 (two "
+                "threads per lane, 64 columns each)",
                 v->num_warps);
+  if (v->num_warps == 8 && v->block_n != 128)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "num_warps=8 splits 128-column S rows in halves; BLOCK_N must be 128");
   if (v->waves_per_eu != 1)
     return fail(B200ATTN_UNSUPPORTED_CONFIG,
                 "waves_per_eu=%d: AMD occupancy hint; one attention CTA owns an SM's TMEM on sm_100a",
@@ -221,10 +230,11 @@ int check_prefill(const b200attn_prefill_params* p, const b200attn_prefill_varia
   const int nq = v->block_m / 128;
   const PrefillEntry* e = nullptr;
   for (const auto& x : kPrefill)
-    if (x.nq == nq && x.bn == v->block_n && x.ns == v->num_stages) e = &x;
+    if (x.nq == nq && x.bn == v->block_n && x.ns == v->num_stages && x.nw == v->num_warps) e = &x;
   if (!e)
-    return fail(B200ATTN_UNSUPPORTED_CONFIG, "no compiled variant for BLOCK_M=%d BLOCK_N=%d num_stages=%d",
-                v->block_m, v->block_n, v->num_stages);
+    return fail(B200ATTN_UNSUPPORTED_CONFIG,
+                "no compiled variant for BLOCK_M=%d BLOCK_N=%d num_warps=%d num_stages=%d", v->block_m,
+                v->block_n, v->num_warps, v->num_stages);
   if (e->smem > kMaxSmem)
     return fail(B200ATTN_SMEM_OVERFLOW, "shared memory %d B > %d B (BLOCK_M=%d BLOCK_N=%d num_stages=%d)",
                 e->smem, kMaxSmem, v->block_m, v->block_n, v->num_stages);

@@ -47,25 +47,50 @@ struct PrefillKernelArgs {
   int32_t speculate;  // 1: interior tiles take the single-pass path against the running max
 };
 
-template <int NQ, int BN, int NSTAGE_CFG>
+// SPLIT = softmax warps per TMEM lane quadrant (num_warps / 4): with SPLIT = 2 two threads share
+// an S row, each owning BN / 2 columns — two warps per SMSP per tile, so one warp's MUFU/FMA
+// dependency stalls are filled by its partner (a single warp reaches ~66% of MUFU.EX2 throughput,
+// two reach ~95%; scripts/probes/mufu_probe.cu).
+template <int NQ, int BN, int NSTAGE_CFG, int SPLIT = 1>
 struct PrefillCfg {
   static constexpr int D = 128;
   static constexpr int BM = 128;
+  static constexpr int NCOL = BN / SPLIT;                    // S columns per softmax thread
   static constexpr int NSLOT = (NSTAGE_CFG + 1) * 128 / BN;  // ring = (num_stages + 1) x 32 KB
-  static constexpr int NUM_SOFTMAX_WARPS = 4 * NQ;
+  static constexpr int NUM_SOFTMAX_WARPS = 4 * NQ * SPLIT;
+  static constexpr int TILE_THREADS = 128 * SPLIT;           // softmax threads per Q tile
   static constexpr int TMA_WARP = NUM_SOFTMAX_WARPS;
   static constexpr int MMA_WARP = NUM_SOFTMAX_WARPS + 1;
-  static constexpr int NTHREADS = 32 * (NUM_SOFTMAX_WARPS + 2);
+  // Registers: the register file is split per SMSP (16K each) and warp w runs on SMSP w % 4, so
+  // each SMSP holds NQ * SPLIT softmax warps + one producer-side warp.  When that leaves the softmax
+  // warps short of registers, the producer side is padded to a full warpgroup (TMA, MMA, 2 idle
+  // warps) that gives its registers to the softmax warpgroups with setmaxnreg.
+  static constexpr int SM_PER_SMSP = NQ * SPLIT;
+  static constexpr bool REG_SPLIT = SM_PER_SMSP == 2;  // at 4 per SMSP ptxas cannot fit the softmax in 120
+  static constexpr int NTHREADS = 32 * (NUM_SOFTMAX_WARPS + (REG_SPLIT ? 4 : 2));
+  // setmaxnreg moves registers within the CTA's launch allocation (NTHREADS x the launch-bound
+  // count, 65536 / NTHREADS rounded down to 8); an .inc beyond what the .dec warps released blocks
+  // forever, so the softmax count is derived from that pool
+  static constexpr int REG_LAUNCH = ((65536 / NTHREADS) & ~7) > 255 ? 248 : ((65536 / NTHREADS) & ~7);
+  static constexpr int REG_OTHER = 64;
+  static constexpr int REG_SOFTMAX_RAW = ((NTHREADS * REG_LAUNCH - 128 * REG_OTHER) / (32 * NUM_SOFTMAX_WARPS)) & ~7;
+  static constexpr int REG_SOFTMAX = REG_SOFTMAX_RAW > 248 ? 248 : REG_SOFTMAX_RAW;
+  static_assert(!REG_SPLIT || (REG_SOFTMAX >= REG_LAUNCH &&
+                               32 * NUM_SOFTMAX_WARPS * REG_SOFTMAX + 128 * REG_OTHER <= NTHREADS * REG_LAUNCH),
+                "setmaxnreg split exceeds the launch allocation");
   static constexpr int Q_BYTES = BM * D * 2;   // 32 KB per Q tile (2 SW128 halves)
   static constexpr int KV_BYTES = BN * D * 2;  // one K or V tile
   static constexpr int HALF_Q = BM * 128;
   static constexpr int HALF_KV = BN * 128;
   // Q is double-buffered when the ring leaves room: the next item's Q lands during this item
-  static constexpr int QBUF = (2 * NQ * Q_BYTES + (NSTAGE_CFG + 1) * 32768 <= 229376) ? 2 : 1;
+  // SPLIT = 2: per-row exchange of half-row maxima (by step parity) and half-row sums
+  static constexpr int XCH_FLOATS = (SPLIT > 1) ? 3 * NQ * SPLIT * 128 : 0;
+  static constexpr int QBUF = (2 * NQ * Q_BYTES + (NSTAGE_CFG + 1) * 32768 + XCH_FLOATS * 4 <= 229376) ? 2 : 1;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = OFF_Q + QBUF * NQ * Q_BYTES;
   static constexpr int OFF_ITEM = OFF_KV + NSLOT * KV_BYTES;  // int32[2] work-item mailbox
-  static constexpr int OFF_BAR = OFF_ITEM + 16;
+  static constexpr int OFF_XCH = OFF_ITEM + 16;
+  static constexpr int OFF_BAR = OFF_XCH + XCH_FLOATS * 4;
   // S_t is double-buffered when TMEM has room (NQ = 2 with BLOCK_N = 64, or NQ = 1): QK_t then runs
   // two KV steps ahead of PV_t, so the softmax of step j+1 never waits for PV_t(j) + QK_t(j+1)
   static constexpr int SB = (NQ * 2 * BN + NQ * 128 <= 512) ? 2 : 1;  // S buffers per tile
@@ -78,6 +103,7 @@ struct PrefillCfg {
   __host__ __device__ static constexpr uint32_t S_COL(int t, int b) { return (t * SB + b) * BN; }
   __host__ __device__ static constexpr uint32_t O_COL(int t) { return NQ * SB * BN + t * 128; }
   static_assert(BN == 64 || BN == 128, "BLOCK_N in {64,128}");
+  static_assert(SPLIT == 1 || (SPLIT == 2 && BN == 128), "two threads per row need 64-column halves");
 };
 
 // 2^x on the FMA pipe (x <= 0): round-to-nearest split x = n + f, f in [-0.5, 0.5], degree-3
@@ -219,8 +245,9 @@ __device__ __forceinline__ float softmax_rowmax(uint32_t s_addr, int kv0, int li
 // stays in registers and is stored unless a row sum passed 2^64 (then, rarely, the caller redoes
 // the tile with the exact two-pass path, S still intact in TMEM).  Saves the max pass (a second
 // TMEM read, its load latency and 0.5 FMNMX per score) on nearly every tile.
-template <int BN, int EMU>
-__device__ __forceinline__ bool softmax_speculative(uint32_t s_addr, float sl2, float m_run, float& lsum) {
+template <int BN, int EMU, int SPLIT>
+__device__ __forceinline__ bool softmax_speculative(uint32_t s_addr, float sl2, float m_run, float& lsum,
+                                                    uint32_t pair_bar) {
   float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   uint32_t pk[BN / 2];
   const float nmu = -m_run;
@@ -254,7 +281,12 @@ __device__ __forceinline__ bool softmax_speculative(uint32_t s_addr, float sl2, 
   fadd2(ls[4], ls[5], ls[6], ls[7]);
   fadd2(ls[0], ls[1], ls[4], ls[5]);
   lsum = ls[0] + ls[1];
-  if (!__all_sync(0xffffffffu, m_run != -INFINITY && lsum <= 1.8446744e19f)) return false;  // 2^64
+  const bool ok = m_run != -INFINITY && lsum <= 1.8446744e19f;  // 2^64
+  if constexpr (SPLIT == 1) {
+    if (!__all_sync(0xffffffffu, ok)) return false;
+  } else {
+    if (!named_bar_and(pair_bar, 32 * SPLIT, ok)) return false;  // both owners of the rows redo, or neither
+  }
 #pragma unroll
   for (int g = 0; g < BN / 32; ++g) tmem_st16(s_addr + g * 16, *reinterpret_cast<const uint32_t(*)[16]>(pk + g * 16));
   return true;
@@ -273,18 +305,19 @@ __device__ unsigned long long g_trace[16][512];  // 8..11: P done by warp 0..3 o
   } while (0)
 #endif
 
-template <int NQ, int BN, int NSTAGE_CFG, int EMU>
-__global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
+template <int NQ, int BN, int NSTAGE_CFG, int EMU, int SPLIT>
+__global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREADS, 1)
     prefill_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
                        const __grid_constant__ CUtensorMap tmap_v, const PrefillKernelArgs args) {
-  using C = PrefillCfg<NQ, BN, NSTAGE_CFG>;
-  constexpr int D = C::D, BM = C::BM, NS = C::NSLOT;
+  using C = PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>;
+  constexpr int D = C::D, BM = C::BM, NS = C::NSLOT, NCOL = C::NCOL;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem + C::OFF_Q;
   uint8_t* sKV = smem + C::OFF_KV;
   volatile int32_t* item_box = reinterpret_cast<volatile int32_t*>(smem + C::OFF_ITEM);
+  float* xch = reinterpret_cast<float*>(smem + C::OFF_XCH);  // [3][NQ][SPLIT][128]: max (2 parities), sum
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars;       // [2]
   uint64_t* q_empty = bars + 2;  // [2]
@@ -314,15 +347,15 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
     }
     for (int t = 0; t < NQ; ++t) {
       for (int b = 0; b < C::SB; ++b) mbar_init(&s_full[t * C::SB + b], 1);
-      mbar_init(&p_full[2 * t], 128);
-      mbar_init(&p_full[2 * t + 1], 128);
+      mbar_init(&p_full[2 * t], C::TILE_THREADS);
+      mbar_init(&p_full[2 * t + 1], C::TILE_THREADS);
       mbar_init(&o_done[2 * t], 1);
       mbar_init(&o_done[2 * t + 1], 1);
-      mbar_init(&o_free[t], 128);
+      mbar_init(&o_free[t], C::TILE_THREADS);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&item_full[i], 1);
-      mbar_init(&item_empty[i], 1 + 128 * NQ);
+      mbar_init(&item_empty[i], 1 + C::TILE_THREADS * NQ);
     }
     fence_barrier_init();
   }
@@ -331,6 +364,11 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // register hand-over (REG_SPLIT): each role adjusts its own limit at the top of its branch, so
+  // the allocator never sees a join of the two limits
+  auto regs_other = [] {
+    if constexpr (C::REG_SPLIT) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::REG_OTHER));
+  };
 
   auto n_kv_of = [&](int seq_len, int qblk) {
     const int kv_end = args.causal ? min(seq_len, qblk * BM + BM) : seq_len;
@@ -339,6 +377,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
 
   if (warp == C::TMA_WARP) {
     // ------------------------------------------------------------ scheduler + TMA producer
+    regs_other();
     if (lane == 0) {
       tma_prefetch_desc(&tmap_q);
       tma_prefetch_desc(&tmap_k);
@@ -381,6 +420,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
     }
   } else if (warp == C::MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer (whole warp, one elected lane issues)
+    regs_other();
     {
       constexpr uint32_t IDESC_QK = idesc_bf16_f32(BM, BN, false, false);
       constexpr uint32_t IDESC_PV = idesc_bf16_f32(BM, D, false, true);
@@ -400,7 +440,9 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
       auto issue_pv = [&](int t, int slot, int buf, bool acc) {
         const uint64_t vb = v_desc + ((slot * C::KV_BYTES) >> 4);
         if constexpr (BN == 128) {
-          umma_ts_k128<128, 512>(tmem + C::O_COL(t), tmem + C::S_COL(t, buf), vb, IDESC_PV, acc ? 1u : 0u);
+          // SPLIT = 2: P of S columns [64, 128) sits at S column 64 (the second half-row owner's range)
+          umma_ts_k128<128, 512, (SPLIT == 2 ? 32 : 0)>(tmem + C::O_COL(t), tmem + C::S_COL(t, buf), vb, IDESC_PV,
+                                                       acc ? 1u : 0u);
         } else {
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
@@ -461,13 +503,21 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
         gt += n_kv;
       }
     }
-  } else {
-    // ------------------------------------------------------------ softmax warpgroup t
-    const int t = warp >> 2;
+  } else if (warp < C::NUM_SOFTMAX_WARPS) {
+    // ------------------------------------------------------------ softmax warps of tile t
+    if constexpr (C::REG_SPLIT) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::REG_SOFTMAX));
+    // warp = (t * SPLIT + hh) * 4 + quadrant: the thread owns S row `row`, columns [hh*NCOL, +NCOL),
+    // and O columns [hh*128/SPLIT, +128/SPLIT).  With SPLIT = 2 the two owners of a row sit on the
+    // same SMSP and agree on every per-row decision through the pair barrier (named, 64 threads).
+    const int t = warp / (4 * SPLIT);
+    const int hh = (warp >> 2) % SPLIT;
     const int row = ((warp & 3) << 5) + lane;  // query row within the block == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) << 5) << 16;
-    const uint32_t s_base = tmem + lane_base;
-    const uint32_t o_addr = tmem + lane_base + C::O_COL(t);
+    const uint32_t s_base = tmem + lane_base + hh * NCOL;
+    constexpr int OCOLS = 128 / SPLIT;
+    const uint32_t o_addr = tmem + lane_base + C::O_COL(t) + hh * OCOLS;
+    const uint32_t pair_bar = 1 + t * 4 + (warp & 3);
+    auto xidx = [&](int k, int h) { return ((k * NQ + t) * SPLIT + h) * 128 + row; };
     const float sl2 = args.scale_log2;
     int gt = 0;
     for (int k = 0;; ++k) {
@@ -490,25 +540,36 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
         mbar_wait(&s_full[t * C::SB + buf], ((gt + j) / C::SB) & 1);
         tc_fence_after();
         const uint32_t s_addr = s_base + C::S_COL(t, buf);
-        if (row == 0) TRACE(t, gt + j);
-        if (t == 0 && lane == 0) TRACE(12 + warp, gt + j);
+        if (row == 0 && hh == 0) TRACE(t, gt + j);
+        if (t == 0 && lane == 0 && warp < 4) TRACE(12 + warp, gt + j);
         const int kv0 = j * BN;
+        const int kv0h = kv0 + hh * NCOL;  // first key of this thread's columns
         const bool edge = (kv0 + BN > kv_end) || (args.causal && kv0 + BN - 1 > q_pos);
-        // masking is only needed on the diagonal / last tile: decide per warp, keep the common
-        // path free of per-element compares and selects
+        // masking is only needed on the diagonal / last tile: decide per warp (and, being a
+        // function of the rows only, identically for both owners of a row), keep the common path
+        // free of per-element compares and selects
         const bool warp_edge = __any_sync(0xffffffffu, edge);
         float lsum_spec;
-        if (args.speculate && j > 0 && !warp_edge && softmax_speculative<BN, EMU>(s_addr, sl2, m_run, lsum_spec)) {
+        if (args.speculate && j > 0 && !warp_edge &&
+            softmax_speculative<NCOL, EMU, SPLIT>(s_addr, sl2, m_run, lsum_spec, pair_bar)) {
           l_run += lsum_spec;
           tmem_wait_st();
           tc_fence_before();
-          if (row == 0) TRACE(2 + t, gt + j);
-          if (t == 0 && lane == 0) TRACE(8 + warp, gt + j);
+          if (row == 0 && hh == 0) TRACE(2 + t, gt + j);
+          if (t == 0 && lane == 0 && warp < 4) TRACE(8 + warp, gt + j);
           mbar_arrive(&p_full[2 * t + ((gt + j) & 1)]);
           continue;
         }
-        const float mt = warp_edge ? softmax_rowmax<BN, true>(s_addr, kv0, lim)
-                                   : softmax_rowmax<BN, false>(s_addr, kv0, lim);
+        float mt = warp_edge ? softmax_rowmax<NCOL, true>(s_addr, kv0h, lim)
+                             : softmax_rowmax<NCOL, false>(s_addr, kv0h, lim);
+        if constexpr (SPLIT == 2) {
+          // row max = max of the two halves; buffers alternate by step parity, and every step has
+          // at least one pair barrier, so a buffer is never rewritten before the partner read it
+          const int par = (gt + j) & 1;
+          xch[xidx(par, hh)] = mt;
+          named_bar_sync(pair_bar, 64);
+          mt = fmaxf(mt, xch[xidx(par, hh ^ 1)]);
+        }
         const float m_new = fmaxf(m_run, mt * sl2);
         const bool need = (m_new > m_run + 8.0f);
         float alpha = 1.f;
@@ -524,7 +585,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
           mbar_wait(&o_done[2 * t + ((gt + j - 1) & 1)], ((gt + j - 1) >> 1) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < OCOLS / 32; ++c) {
             uint32_t r[32];
             tmem_ld32(o_addr + c * 32, r);
 #pragma unroll
@@ -533,25 +594,31 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
           }
         }
         const float nmu = (m_run == -INFINITY) ? 0.f : -m_run;
-        const float lsum = warp_edge ? softmax_pass2<BN, true, EMU>(s_addr, sl2, nmu, kv0, lim)
-                                     : softmax_pass2<BN, false, EMU>(s_addr, sl2, nmu, kv0, lim);
+        const float lsum = warp_edge ? softmax_pass2<NCOL, true, EMU>(s_addr, sl2, nmu, kv0h, lim)
+                                     : softmax_pass2<NCOL, false, EMU>(s_addr, sl2, nmu, kv0h, lim);
         l_run += lsum;
         tmem_wait_st();
         tc_fence_before();
-        if (row == 0) TRACE(2 + t, gt + j);
-        if (t == 0 && lane == 0) TRACE(8 + warp, gt + j);
+        if (row == 0 && hh == 0) TRACE(2 + t, gt + j);
+        if (t == 0 && lane == 0 && warp < 4) TRACE(8 + warp, gt + j);
         mbar_arrive(&p_full[2 * t + ((gt + j) & 1)]);
       }
 
       // ---------------------------------------------------------- epilogue for this item
+      float l_tot = l_run;
+      if constexpr (SPLIT == 2) {
+        xch[xidx(2, hh)] = l_run;
+        named_bar_sync(pair_bar, 64);
+        l_tot += xch[xidx(2, hh ^ 1)];
+      }
       mbar_wait(&o_done[2 * t + ((gt + n_kv - 1) & 1)], ((gt + n_kv - 1) >> 1) & 1);  // last PV_t
       tc_fence_after();
       const int h = hg * NQ + t;
       const bool valid = q_pos < seq_len;
-      const float inv_l = (l_run > 0.f) ? 1.f / l_run : 0.f;
-      __nv_bfloat16* orow = args.o + (static_cast<size_t>(seq_start + q_pos) * args.num_q_heads + h) * D;
+      const float inv_l = (l_tot > 0.f) ? 1.f / l_tot : 0.f;
+      __nv_bfloat16* orow = args.o + (static_cast<size_t>(seq_start + q_pos) * args.num_q_heads + h) * D + hh * OCOLS;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < OCOLS / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(o_addr + c * 32, r);
         if (valid) {
@@ -566,12 +633,14 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG>::NTHREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(&o_free[t]);
-      if (valid && args.lse != nullptr) {
+      if (valid && hh == 0 && args.lse != nullptr) {
         args.lse[static_cast<size_t>(h) * args.total_tokens + seq_start + q_pos] =
-            (l_run > 0.f) ? (m_run + __log2f(l_run)) * 0.69314718055994530942f : -INFINITY;
+            (l_tot > 0.f) ? (m_run + __log2f(l_tot)) * 0.69314718055994530942f : -INFINITY;
       }
       gt += n_kv;
     }
+  } else {
+    regs_other();  // idle padding warps of the producer warpgroup
   }
 
   tc_fence_before();

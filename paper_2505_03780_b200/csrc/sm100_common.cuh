@@ -88,6 +88,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// Named barrier that also ANDs a predicate over the participating threads.
+__device__ __forceinline__ bool named_bar_and(uint32_t id, uint32_t nthreads, bool pred) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "bar.red.and.pred q, %2, %3, p;\n\t"
+      "selp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"((uint32_t)pred), "r"(id), "r"(nthreads)
+      : "memory");
+  return r != 0;
+}
 
 // Generic-proxy smem writes -> visible to the async proxy (tensor core / TMA).
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -250,8 +263,10 @@ __device__ __forceinline__ void umma_ss_k128(uint32_t d, uint64_t a, uint64_t b,
       : "memory");
 }
 
-// TS variant: A from TMEM, step kk at a_tmem + 8 kk (16 bf16 = 8 columns); B as above.
-template <int BS, int BH>
+// TS variant: A from TMEM, step kk at a_tmem + 8 kk + (kk >= 4 ? AGAP : 0) (16 bf16 = 8 columns;
+// AGAP > 0 when the two 64-row K halves of P were written by different warps into their own S
+// column ranges); B as above.
+template <int BS, int BH, int AGAP = 0>
 __device__ __forceinline__ void umma_ts_k128(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile("{\n\t.reg .pred e, p;\n\t.reg .b32 ta;\n\t.reg .b64 tb;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
@@ -264,16 +279,17 @@ __device__ __forceinline__ void umma_ts_k128(uint32_t d, uint32_t a_tmem, uint64
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
       "add.s32 ta, %1, 24;\n\tadd.s64 tb, %2, %7;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
-      "add.s32 ta, %1, 32;\n\tadd.s64 tb, %2, %8;\n\t"
+      "add.s32 ta, %1, %12;\n\tadd.s64 tb, %2, %8;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
-      "add.s32 ta, %1, 40;\n\tadd.s64 tb, %2, %9;\n\t"
+      "add.s32 ta, %1, %13;\n\tadd.s64 tb, %2, %9;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
-      "add.s32 ta, %1, 48;\n\tadd.s64 tb, %2, %10;\n\t"
+      "add.s32 ta, %1, %14;\n\tadd.s64 tb, %2, %10;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
-      "add.s32 ta, %1, 56;\n\tadd.s64 tb, %2, %11;\n\t"
+      "add.s32 ta, %1, %15;\n\tadd.s64 tb, %2, %11;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
       "}"
-      :: "r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "n"(((1 & 3) * BS + (1 >> 2) * BH)), "n"(((2 & 3) * BS + (2 >> 2) * BH)), "n"(((3 & 3) * BS + (3 >> 2) * BH)), "n"(((4 & 3) * BS + (4 >> 2) * BH)), "n"(((5 & 3) * BS + (5 >> 2) * BH)), "n"(((6 & 3) * BS + (6 >> 2) * BH)), "n"(((7 & 3) * BS + (7 >> 2) * BH))
+      :: "r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "n"(((1 & 3) * BS + (1 >> 2) * BH)), "n"(((2 & 3) * BS + (2 >> 2) * BH)), "n"(((3 & 3) * BS + (3 >> 2) * BH)), "n"(((4 & 3) * BS + (4 >> 2) * BH)), "n"(((5 & 3) * BS + (5 >> 2) * BH)), "n"(((6 & 3) * BS + (6 >> 2) * BH)), "n"(((7 & 3) * BS + (7 >> 2) * BH)),
+         "n"(32 + AGAP), "n"(40 + AGAP), "n"(48 + AGAP), "n"(56 + AGAP)
       : "memory");
 }
 

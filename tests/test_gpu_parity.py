@@ -29,8 +29,8 @@ ROOT = Path(__file__).resolve().parents[1]
 DEV = "cuda"
 
 
-def pcfg(bm=256, bn=128, ns=3, pre=False):
-    return dict(BLOCK_M=bm, BLOCK_N=bn, num_warps=4, num_stages=ns, waves_per_eu=1, PRE_LOAD_V=pre)
+def pcfg(bm=256, bn=128, ns=3, pre=False, nw=4):
+    return dict(BLOCK_M=bm, BLOCK_N=bn, num_warps=nw, num_stages=ns, waves_per_eu=1, PRE_LOAD_V=pre)
 
 
 def dcfg(splits=0, ns=4, tile=128):
@@ -163,8 +163,9 @@ def test_prefill_causal(lens):
     check(f"prefill {lens}", out, ref, base)
 
 
+@pytest.mark.parametrize("nw", [4, 8])
 @pytest.mark.parametrize("boost", [6.0, 40.0])
-def test_prefill_score_jumps_after_first_tile(boost):
+def test_prefill_score_jumps_after_first_tile(boost, nw):
     """Keys past the first 2 KV tiles are scaled up so later tiles' scores exceed the running max
     from the first tile by ~20 (boost 6: the speculative single pass keeps P = 2^(s - m_run) up to
     2^20 in bf16) or by > 64 (boost 40: the row sum passes 2^64 and the tile is redone exactly)."""
@@ -180,14 +181,15 @@ def test_prefill_score_jumps_after_first_tile(boost):
     cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32)
     ref = oracle.prefill(q, k, v, cu)
     qd, kd, vd = q.to(DEV), k.to(DEV), v.to(DEV)
-    out = A.prefill_varlen(qd, kd, vd, cu.to(DEV), max(lens), config=pcfg())
+    out = A.prefill_varlen(qd, kd, vd, cu.to(DEV), max(lens), config=pcfg(ns=2 if nw == 8 else 3, nw=nw))
     assert not torch.isnan(out).any()
-    check(f"prefill score jumps x{boost}", out, ref, sdpa_prefill_bf16(qd, kd, vd, cu, True))
+    check(f"prefill score jumps x{boost} w{nw}", out, ref, sdpa_prefill_bf16(qd, kd, vd, cu, True))
 
 
-def test_prefill_noncausal():
-    out, ref, base = run_prefill([200, 64, 129], causal=False)
-    check("prefill noncausal", out, ref, base)
+@pytest.mark.parametrize("nw", [4, 8])
+def test_prefill_noncausal(nw):
+    out, ref, base = run_prefill([200, 64, 129], causal=False, cfg=pcfg(ns=2, nw=nw))
+    check(f"prefill noncausal w{nw}", out, ref, base)
 
 
 @pytest.mark.parametrize("hq,hkv", [(8, 8), (16, 2), (32, 8), (64, 8)])
@@ -197,13 +199,14 @@ def test_prefill_gqa_shapes(hq, hkv):
     check(f"prefill gqa {hq}/{hkv}", out, ref, base)
 
 
-VARIANTS = [(bm, bn, ns) for bm in (128, 256) for bn in (64, 128) for ns in (1, 2, 3, 4)]
+VARIANTS = [(bm, bn, ns, 4) for bm in (128, 256) for bn in (64, 128) for ns in (1, 2, 3, 4)] + \
+    [(bm, 128, ns, 8) for bm in (128, 256) for ns in (1, 2)]
 
 
-@pytest.mark.parametrize("bm,bn,ns", VARIANTS)
-def test_prefill_every_compiled_variant(bm, bn, ns):
-    out, ref, base = run_prefill([300, 77, 129], cfg=pcfg(bm, bn, ns))
-    check(f"prefill variant {bm}/{bn}/{ns}", out, ref, base)
+@pytest.mark.parametrize("bm,bn,ns,nw", VARIANTS)
+def test_prefill_every_compiled_variant(bm, bn, ns, nw):
+    out, ref, base = run_prefill([300, 77, 129], cfg=pcfg(bm, bn, ns, nw=nw))
+    check(f"prefill variant {bm}/{bn}/{ns}/w{nw}", out, ref, base)
 
 
 def test_prefill_lse():

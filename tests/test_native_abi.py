@@ -50,12 +50,17 @@ def test_prefill_supported_accepts_compiled_variants():
             for ns in (1, 2, 3, 4):
                 rc, why = A.prefill_supported(config=cfg(BLOCK_M=bm, BLOCK_N=bn, num_stages=ns), **C1)
                 assert rc == _native.OK, why
+        for ns in (1, 2):  # two softmax threads per S row
+            rc, why = A.prefill_supported(config=cfg(BLOCK_M=bm, num_warps=8, num_stages=ns), **C1)
+            assert rc == _native.OK, why
 
 
 @pytest.mark.parametrize("kw,code", [
     (dict(BLOCK_M=64), _native.UNSUPPORTED_CONFIG),
     (dict(BLOCK_N=32, BLOCK_M=128), _native.UNSUPPORTED_CONFIG),
-    (dict(num_warps=8), _native.UNSUPPORTED_CONFIG),
+    (dict(num_warps=2), _native.UNSUPPORTED_CONFIG),
+    (dict(num_warps=8, num_stages=3), _native.UNSUPPORTED_CONFIG),
+    (dict(num_warps=8, num_stages=2, BLOCK_N=64), _native.UNSUPPORTED_CONFIG),
     (dict(waves_per_eu=2), _native.UNSUPPORTED_CONFIG),
     (dict(num_stages=5), _native.UNSUPPORTED_CONFIG),
 ])
@@ -81,8 +86,9 @@ def test_flash_attention_space_variant_map():
         ok += rc == _native.OK
         if rc != _native.OK:
             assert why
-    # BLOCK_M {128,256} x BLOCK_N {64,128} x num_stages 1..4 (x PRE_LOAD_V, which needs stages <= 2)
-    assert ok == 24
+    # num_warps 4: BLOCK_M {128,256} x BLOCK_N {64,128} x num_stages 1..4 (x PRE_LOAD_V, which needs
+    # stages <= 2) = 24; num_warps 8: BLOCK_M {128,256} x BLOCK_N 128 x num_stages {1,2} x PRE_LOAD_V = 8
+    assert ok == 32
 
 
 def test_decode_supported_and_splits():
