@@ -53,7 +53,7 @@ typedef enum {
 typedef struct {
   int32_t block_m;      /* BLOCK_M: query rows per CTA summed over its q heads: 128 (1 tile) | 256 (head pair) */
   int32_t block_n;      /* BLOCK_N: KV rows per pipeline step: 64 | 128                                         */
-  int32_t num_warps;    /* softmax warps per 128-row Q tile: 4 (one thread per TMEM lane)                        */
+  int32_t num_warps;    /* softmax warps per 128-row Q tile: 4 (one thread per TMEM lane) or 8 (two, BLOCK_N 128) */
   int32_t num_stages;   /* K/V ring = (num_stages + 1) x 32 KB of TMA slots (BLOCK_N rows of K or V each)         */
   int32_t waves_per_eu; /* AMD occupancy hint; only 1 is meaningful on sm_100a                                   */
   int32_t pre_load_v;   /* V_j is always issued right behind K_j on the shared ring; accepted for parity         */
