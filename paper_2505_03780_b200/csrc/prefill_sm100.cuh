@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
       const uint64_t keep = policy_evict_last();  // K/V tiles are re-read by other q blocks / heads
       int ri = 0;
       for (int k = 0;; ++k) {
-        if (k >= 2) mbar_wait(&item_empty[k & 1], ((k >> 1) - 1) & 1);
+        if (k >= 2) mbar_wait_producer(&item_empty[k & 1], ((k >> 1) - 1) & 1);
         int w = atomicAdd(args.sched, 1);
         if (w >= total_work) w = -1;
         item_box[k & 1] = w;
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
         const int n_kv = n_kv_of(seq_len, qblk);
         const int qb = (C::QBUF == 2) ? (k & 1) : 0;
         const uint32_t qph = (C::QBUF == 2) ? ((k >> 1) & 1) : (k & 1);
-        mbar_wait(&q_empty[qb], qph ^ 1);
+        mbar_wait_producer(&q_empty[qb], qph ^ 1);
         mbar_arrive_expect_tx(&q_full[qb], NQ * C::Q_BYTES);
         for (int t = 0; t < NQ; ++t)
           for (int hf = 0; hf < 2; ++hf)
@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
                         seq_start + qblk * BM);
         for (int idx = 0; idx < 2 * n_kv; ++idx, ++ri) {
           const int slot = ri % NS;
-          mbar_wait(&kv_empty[slot], ((ri / NS) & 1) ^ 1);
+          mbar_wait_producer(&kv_empty[slot], ((ri / NS) & 1) ^ 1);
           const CUtensorMap* map = (idx & 1) ? &tmap_v : &tmap_k;
           uint8_t* dst = sKV + slot * C::KV_BYTES;
           mbar_arrive_expect_tx(&kv_full[slot], C::KV_BYTES);
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
       // ring positions follow the TMA's load order: K_s at rbase + 2s, V_s at rbase + 2s + 1
       int rbase = 0, gt = 0;
       for (int k = 0;; ++k) {
-        mbar_wait(&item_full[k & 1], (k >> 1) & 1);
+        mbar_wait_producer(&item_full[k & 1], (k >> 1) & 1);
         const int w = item_box[k & 1];
         __syncwarp();
         if (lane == 0) mbar_arrive(&item_empty[k & 1]);  // the MMA warp counts as one consumer
@@ -463,12 +463,12 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
         const int seq_start = args.cu_seqlens[seq];
         const int n_kv = n_kv_of(args.cu_seqlens[seq + 1] - seq_start, qblk);
         qb = (C::QBUF == 2) ? (k & 1) : 0;
-        mbar_wait(&q_full[qb], (C::QBUF == 2) ? ((k >> 1) & 1) : (k & 1));
+        mbar_wait_producer(&q_full[qb], (C::QBUF == 2) ? ((k >> 1) & 1) : (k & 1));
         // QK_t(s) of step s for tile t; per tile, step s uses S buffer (gt + s) % SB
         auto qk_step_tile = [&](int s, int t) {
           const int ki = rbase + 2 * s, kslot = ki % NS;
           if (t == 0) {
-            mbar_wait(&kv_full[kslot], (ki / NS) & 1);
+            mbar_wait_producer(&kv_full[kslot], (ki / NS) & 1);
             tc_fence_after();
           }
           const int buf = (gt + s) % SB;
@@ -483,12 +483,12 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
           for (int t = 0; t < NQ; ++t) qk_step_tile(s, t);
         for (int j = 0; j < n_kv; ++j) {
           const int vi = rbase + 2 * j + 1, vslot = vi % NS;
-          mbar_wait(&kv_full[vslot], (vi / NS) & 1);
+          mbar_wait_producer(&kv_full[vslot], (vi / NS) & 1);
           TRACE(6, gt + j);
           for (int t = 0; t < NQ; ++t) {
-            mbar_wait(&p_full[2 * t + ((gt + j) & 1)], ((gt + j) >> 1) & 1);
+            mbar_wait_producer(&p_full[2 * t + ((gt + j) & 1)], ((gt + j) >> 1) & 1);
             TRACE(4 + t, gt + j);
-            if (j == 0 && k > 0) mbar_wait(&o_free[t], (k - 1) & 1);
+            if (j == 0 && k > 0) mbar_wait_producer(&o_free[t], (k - 1) & 1);
             tc_fence_after();
             issue_pv(t, vslot, (gt + j) % SB, j > 0);
             umma_commit_w(&o_done[2 * t + ((gt + j) & 1)]);

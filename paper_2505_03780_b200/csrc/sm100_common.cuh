@@ -83,6 +83,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (++spins == B200_WAIT_TRAP_SPINS) __trap();
   }
 }
+#ifndef B200_PRODUCER_SLEEP_NS
+#define B200_PRODUCER_SLEEP_NS 0  // > 0: producer-side (TMA / MMA warp) waits back off with nanosleep
+#endif
+// Wait used by warps that share an SMSP with softmax warps but have no arithmetic of their own:
+// optionally yields the issue slot between polls.
+__device__ __forceinline__ void mbar_wait_producer(uint64_t* bar, uint32_t parity) {
+#if B200_PRODUCER_SLEEP_NS > 0
+  const uint32_t a = smem_u32(bar);
+  uint32_t spins = 0;
+  while (!mbar_try_wait(a, parity)) {
+    if (++spins == B200_WAIT_TRAP_SPINS) __trap();
+    __nanosleep(B200_PRODUCER_SLEEP_NS);
+  }
+#else
+  mbar_wait(bar, parity);
+#endif
+}
 
 // Named barrier among a subset of warps (ids 1..15; 0 is __syncthreads).
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
