@@ -192,11 +192,12 @@ def test_prefill_noncausal(nw):
     check(f"prefill noncausal w{nw}", out, ref, base)
 
 
+@pytest.mark.parametrize("nw", [4, 8])
 @pytest.mark.parametrize("hq,hkv", [(8, 8), (16, 2), (32, 8), (64, 8)])
-def test_prefill_gqa_shapes(hq, hkv):
-    cfg = pcfg(bm=128) if (hq // hkv) % 2 else pcfg()
+def test_prefill_gqa_shapes(hq, hkv, nw):
+    cfg = pcfg(bm=128, ns=2, nw=nw) if (hq // hkv) % 2 else pcfg(ns=2, nw=nw)
     out, ref, base = run_prefill([300, 17], Hq=hq, Hkv=hkv, cfg=cfg)
-    check(f"prefill gqa {hq}/{hkv}", out, ref, base)
+    check(f"prefill gqa {hq}/{hkv} w{nw}", out, ref, base)
 
 
 VARIANTS = [(bm, bn, ns, 4) for bm in (128, 256) for bn in (64, 128) for ns in (1, 2, 3, 4)] + \
@@ -209,15 +210,17 @@ def test_prefill_every_compiled_variant(bm, bn, ns, nw):
     check(f"prefill variant {bm}/{bn}/{ns}/w{nw}", out, ref, base)
 
 
-def test_prefill_lse():
+@pytest.mark.parametrize("cfg", [None, pcfg(256, 128, 2, nw=8), pcfg(128, 128, 1, nw=8)], ids=["default", "bm256w8", "bm128w8"])
+def test_prefill_lse(cfg):
     lens = [100, 257]
     g = torch.Generator().manual_seed(3)
     T = sum(lens)
     q, k, v = (torch.randn(T, h, 128, generator=g).bfloat16() for h in (8, 2, 2))
     cu = torch.tensor([0, 100, 357], dtype=torch.int32)
     ref, ref_lse = oracle.prefill(q, k, v, cu, with_lse=True)
-    out, lse = A.prefill_varlen(q.to(DEV), k.to(DEV), v.to(DEV), cu.to(DEV), 257, return_lse=True)
+    out, lse = A.prefill_varlen(q.to(DEV), k.to(DEV), v.to(DEV), cu.to(DEV), 257, return_lse=True, config=cfg)
     assert np.abs(lse.cpu().numpy() - ref_lse).max() < 2e-3
+    assert np.abs(out.float().cpu().numpy() - ref).max() < 2e-2
 
 
 def test_prefill_c1_full():
@@ -228,11 +231,13 @@ def test_prefill_c1_full():
     check("C1 full", out, ref, sdpa_prefill_bf16(qd, kd, vd, x.cu_seqlens, True))
 
 
-def test_prefill_c3_full_size_subset():
+@pytest.mark.parametrize("cfg", [None, pcfg(256, 128, 2, nw=8)], ids=["dispatch", "bm256w8"])
+def test_prefill_c3_full_size_subset(cfg):
     """Run all of C3 (16 seqs, 33430 tokens) on the GPU; check the shortest, a middle and the
     longest sequence on kv heads {0, 7} (their 8 q heads) against the oracle."""
     x = W.make_prefill(W.C3, device="cpu")
-    out = A.prefill_varlen(x.q.to(DEV), x.k.to(DEV), x.v.to(DEV), x.cu_seqlens.to(DEV), x.max_seqlen).cpu()
+    out = A.prefill_varlen(x.q.to(DEV), x.k.to(DEV), x.v.to(DEV), x.cu_seqlens.to(DEV), x.max_seqlen,
+                           config=cfg).cpu()
     cu = x.cu_seqlens.tolist()
     for s in (0, 8, 15):
         a, b = cu[s], cu[s + 1]
