@@ -34,14 +34,14 @@ _TEMPLATE = re.compile(r"b200(\d+)([a-z_]+)ILi(\d+)ELi(\d+)E(?:Li(\d+)E)?(?:Li(\
 
 
 def variant_id(mangled: str) -> str | None:
-    """prefill_fwd_kernel<NQ,BN,NS,EMU> -> prefill_BM{128*NQ}_BN{BN}_S{NS};
-    decode_flat_kernel<G,NS> -> decode_T16_G{G}_S{NS}; decode_split_kernel<NS> -> decode_T128_S{NS}."""
-    m = re.search(r"prefill_fwd_kernelILi(\d+)ELi(\d+)ELi(\d+)E", mangled)
+    """prefill_fwd_kernel<NQ,BN,NS,EMU,SPLIT> -> prefill_BM{128*NQ}_BN{BN}_S{NS}_W{4*SPLIT};
+    decode_flat_kernel<G,NS,FP8> -> decode_T16_G{G}_S{NS}[_fp8]; decode_split_kernel<NS> -> decode_T128_S{NS}."""
+    m = re.search(r"prefill_fwd_kernelILi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)E", mangled)
     if m:
-        return f"prefill_BM{128 * int(m.group(1))}_BN{m.group(2)}_S{m.group(3)}"
-    m = re.search(r"decode_flat_kernelILi(\d+)ELi(\d+)E", mangled)
+        return f"prefill_BM{128 * int(m.group(1))}_BN{m.group(2)}_S{m.group(3)}_W{4 * int(m.group(5))}"
+    m = re.search(r"decode_flat_kernelILi(\d+)ELi(\d+)ELb(\d)E", mangled)
     if m:
-        return f"decode_T16_G{m.group(1)}_S{m.group(2)}"
+        return f"decode_T16_G{m.group(1)}_S{m.group(2)}" + ("_fp8" if m.group(3) == "1" else "")
     m = re.search(r"decode_split_kernelILi(\d+)E", mangled)
     if m:
         return f"decode_T128_S{m.group(1)}"
