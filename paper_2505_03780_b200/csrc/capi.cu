@@ -102,9 +102,9 @@ int num_sms();
 // ------------------------------------------------------------------ prefill variants
 using PrefillLauncher = int (*)(const b200attn_prefill_params*, cudaStream_t);
 #ifndef B200_PREFILL_EMU
-#define B200_PREFILL_EMU 3
+#define B200_PREFILL_EMU 4
 #endif
-constexpr int kPrefillEmu = B200_PREFILL_EMU;  // 1 pair in 3 on the FMA pipe (C3: EMU 0: 987, 3: 1008, 4: 1003, 6: 1004 TFLOP/s)
+constexpr int kPrefillEmu = B200_PREFILL_EMU;  // 1 pair in 4 on the FMA pipe (session 3, setmaxnreg kernel, C3 TFLOP/s x2: EMU 0 1129/1112, 2 1044/1043, 3 1160/1128, 4 1170/1164, 6 1168/1165)
 
 size_t prefill_ws_ints(const b200attn_prefill_params* p, int* nkeys_out) {
   const int nkeys = (p->max_seqlen + 127) / 128;
