@@ -11,10 +11,13 @@
 // out by prefill_schedule_kernel in longest-first order (causal cost = q block index + 1) and
 // pulled by persistent CTAs (one per SM) from an atomic counter.
 //
-//   warps 0..4*NQ-1 : softmax warpgroup(s), one per Q tile; thread = query row (TMEM lane);
+//   warps 0..W-1    : softmax warps (W = 4*NQ*SPLIT), SPLIT per TMEM lane quadrant of each Q
+//                     tile; a thread owns a query row (TMEM lane), or half of it when SPLIT = 2;
 //                     they also run the epilogue (O -> bf16 -> global) of their tile
-//   warp  4*NQ      : scheduler + TMA producer (Q once per item, then K_j / V_j into a ring)
-//   warp  4*NQ+1    : TMEM allocator + single-thread tcgen05.mma issuer
+//   warp  W         : scheduler + TMA producer (Q once per item, then K_j / V_j into a ring)
+//   warp  W+1       : TMEM allocator + single-thread tcgen05.mma issuer
+//   warps W+2, W+3  : idle padding of the producer warpgroup when it hands registers to the
+//                     softmax warps (setmaxnreg, REG_SPLIT)
 //
 // TMEM (512 cols): S_t at [128 t], O_t at [256 + 128 t].  P_t (bf16 pairs) is written back into
 // the first BN/2 columns of S_t (each thread overwrites only S values it has already read) and PV
@@ -48,9 +51,10 @@ struct PrefillKernelArgs {
 };
 
 // SPLIT = softmax warps per TMEM lane quadrant (num_warps / 4): with SPLIT = 2 two threads share
-// an S row, each owning BN / 2 columns — two warps per SMSP per tile, so one warp's MUFU/FMA
-// dependency stalls are filled by its partner (a single warp reaches ~66% of MUFU.EX2 throughput,
-// two reach ~95%; scripts/probes/mufu_probe.cu).
+// an S row, each owning BN / 2 columns — two warps per SMSP per tile.  In isolation that is the
+// faster layout (a 128-column slice: 1053 cycles on two warps vs 1139 on one,
+// scripts/probes/softmax_probe.cu); inside the kernel the tile softmax did not get shorter, and the
+// sweep picks SPLIT = 2 only for some small shapes (DESIGN.md §4 K1).
 template <int NQ, int BN, int NSTAGE_CFG, int SPLIT = 1>
 struct PrefillCfg {
   static constexpr int D = 128;
