@@ -76,7 +76,10 @@ struct PrefillCfg {
   // count, 65536 / NTHREADS rounded down to 8); an .inc beyond what the .dec warps released blocks
   // forever, so the softmax count is derived from that pool
   static constexpr int REG_LAUNCH = ((65536 / NTHREADS) & ~7) > 255 ? 248 : ((65536 / NTHREADS) & ~7);
-  static constexpr int REG_OTHER = 64;
+#ifndef B200_PREFILL_REG_OTHER
+#define B200_PREFILL_REG_OTHER 64
+#endif
+  static constexpr int REG_OTHER = B200_PREFILL_REG_OTHER;  // producer-warpgroup registers
   static constexpr int REG_SOFTMAX_RAW = ((NTHREADS * REG_LAUNCH - 128 * REG_OTHER) / (32 * NUM_SOFTMAX_WARPS)) & ~7;
   static constexpr int REG_SOFTMAX = REG_SOFTMAX_RAW > 248 ? 248 : REG_SOFTMAX_RAW;
   static_assert(!REG_SPLIT || (REG_SOFTMAX >= REG_LAUNCH &&
