@@ -86,38 +86,77 @@ def prefill_varlen(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, cu_seqlens
     waves_per_eu, PRE_LOAD_V); default: the per-shape dispatch table.
     """
     lib = _native.load()
+    _check_prefill_shapes(q, k, v, cu_seqlens, out)
+    with _on(q.device):
+        if out is None:
+            out = torch.empty_like(q)
+        lse = torch.empty(q.shape[1], q.shape[0], device=q.device, dtype=torch.float32) if return_lse else None
+        if config is None:
+            config = default_prefill_config(num_seqs=cu_seqlens.numel() - 1, total_tokens=q.shape[0],
+                                            max_seqlen=int(max_seqlen), num_q_heads=q.shape[1],
+                                            num_kv_heads=k.shape[1], head_dim=q.shape[2], causal=causal)
+        p = _prefill_params(q, k, v, out, cu_seqlens, max_seqlen, softmax_scale, causal, lse)
+        stream = torch.cuda.current_stream(q.device)
+        ws = _workspace(q.device, lib.b200attn_prefill_workspace_size(p), kind="prefill", stream=stream)
+        p.workspace, p.workspace_bytes = ws.data_ptr(), ws.numel()
+        _native.check(lib.b200attn_prefill(p, prefill_variant(config), stream.cuda_stream))
+    return (out, lse) if return_lse else out
+
+
+def _same_device(*ts):
+    dev = ts[0].device
+    for t in ts[1:]:
+        if t is not None and t.device != dev:
+            raise ValueError(f"all tensors must be on {dev}, got one on {t.device}")
+
+
+def _check_prefill_shapes(q, k, v, cu_seqlens, out=None):
     for t, n in ((q, "q"), (k, "k"), (v, "v")):
         _check(t, n, ndim=3)
     _check(cu_seqlens, "cu_seqlens", dtype=torch.int32, ndim=1)
     if k.shape != v.shape or k.shape[0] != q.shape[0] or k.shape[2] != q.shape[2]:
         raise ValueError(f"shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
-    if out is None:
-        out = torch.empty_like(q)
-    else:
+    if k.shape[1] == 0 or q.shape[1] % k.shape[1]:
+        raise ValueError(f"num_q_heads={q.shape[1]} is not a multiple of num_kv_heads={k.shape[1]}")
+    if cu_seqlens.numel() < 2:
+        raise ValueError("cu_seqlens needs at least 2 entries (one sequence)")
+    if out is not None:
         _check(out, "out", ndim=3)
-    lse = torch.empty(q.shape[1], q.shape[0], device=q.device, dtype=torch.float32) if return_lse else None
-    if config is None:
-        config = default_prefill_config(num_seqs=cu_seqlens.numel() - 1, total_tokens=q.shape[0],
-                                        max_seqlen=int(max_seqlen), num_q_heads=q.shape[1],
-                                        num_kv_heads=k.shape[1], head_dim=q.shape[2], causal=causal)
-    p = _prefill_params(q, k, v, out, cu_seqlens, max_seqlen, softmax_scale, causal, lse)
-    ws = _workspace(q.device, lib.b200attn_prefill_workspace_size(p), kind="prefill")
-    p.workspace, p.workspace_bytes = ws.data_ptr(), ws.numel()
-    _native.check(lib.b200attn_prefill(p, prefill_variant(config), torch.cuda.current_stream(q.device).cuda_stream))
-    return (out, lse) if return_lse else out
+        if out.shape != q.shape:
+            raise ValueError(f"out{tuple(out.shape)} must match q{tuple(q.shape)}")
+    _same_device(q, k, v, cu_seqlens, out)
 
 
-_workspaces: dict = {}
+_workspaces: "OrderedDict" = None
+_WS_MAX = 32  # bound: streams come and go in a server; least recently used buffers are dropped
 
 
-def _workspace(device, nbytes: int, kind: str = "decode") -> Optional[torch.Tensor]:
+def _workspace(device, nbytes: int, kind: str = "decode", stream=None) -> Optional[torch.Tensor]:
+    """Scratch for one launch, cached per (device, stream, kind).
+
+    The prefill buffer carries the self-resetting work counter and the decode buffer the split
+    partials that the combine pass reads, so two launches in flight on different streams must not
+    share one (include/b200attn.h: launches are stream-ordered and reentrant).  Launches on ONE
+    stream are ordered, so they can."""
+    global _workspaces
     if nbytes == 0:
         return None
-    key = (device.type, device.index, kind)
+    if _workspaces is None:
+        from collections import OrderedDict
+
+        _workspaces = OrderedDict()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    key = (device.type, device.index, s.cuda_stream, kind)
     buf = _workspaces.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)  # prefill counter must start at 0
+        # zeroed: the prefill work counter must start at 0 (the kernel's last CTA re-zeroes it);
+        # allocated on the stream that uses it, so the caching allocator never hands it to another
+        with torch.cuda.stream(s):
+            buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
         _workspaces[key] = buf
+    _workspaces.move_to_end(key)
+    while len(_workspaces) > _WS_MAX:
+        _workspaces.popitem(last=False)
     return buf
 
 
@@ -168,35 +207,53 @@ def paged_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, 
     device->host sync is needed.
     """
     lib = _native.load()
+    _check_decode_shapes(q, k_cache, v_cache, block_table, seq_lens, out)
+    if max_seq_len is None:
+        max_seq_len = block_table.shape[1] * k_cache.shape[1]
+    with _on(q.device):
+        if out is None:
+            out = torch.empty_like(q)
+        if config is None:
+            config = default_decode_config(batch_size=q.shape[0], seq_len=int(max_seq_len), num_q_heads=q.shape[1],
+                                           num_kv_heads=k_cache.shape[2], head_dim=q.shape[2],
+                                           block_size=k_cache.shape[1], kv_dtype=_kv_name(k_cache))
+        var = decode_variant(config)
+        p = _decode_params(q, k_cache, v_cache, block_table, seq_lens, out, max_seq_len, softmax_scale,
+                           k_scale=k_scale, v_scale=v_scale)
+        nbytes = lib.b200attn_decode_workspace_size(p, var)
+        stream = torch.cuda.current_stream(q.device)
+        ws = _workspace(q.device, nbytes, kind="decode", stream=stream)
+        if ws is not None:
+            p.workspace = ws.data_ptr()
+            p.workspace_bytes = ws.numel()
+        _native.check(lib.b200attn_decode(p, var, stream.cuda_stream))
+    return out
+
+
+def _check_decode_shapes(q, k_cache, v_cache, block_table, seq_lens, out=None):
+    """Cross-tensor checks: a mismatch here would otherwise be an out-of-bounds device access."""
     _check(q, "q", ndim=3)
     _check_cache(k_cache, "k_cache")
     _check_cache(v_cache, "v_cache")
     if k_cache.dtype != v_cache.dtype:
         raise TypeError("k_cache / v_cache dtype mismatch")
-    _check(block_table, "block_table", dtype=torch.int32, ndim=2)
-    _check(seq_lens, "seq_lens", dtype=torch.int32, ndim=1)
     if k_cache.shape != v_cache.shape:
         raise ValueError("k_cache / v_cache shape mismatch")
-    if max_seq_len is None:
-        max_seq_len = block_table.shape[1] * k_cache.shape[1]
-    if out is None:
-        out = torch.empty_like(q)
-    else:
+    _check(block_table, "block_table", dtype=torch.int32, ndim=2)
+    _check(seq_lens, "seq_lens", dtype=torch.int32, ndim=1)
+    B, Hq, D = q.shape
+    if k_cache.shape[3] != D:
+        raise ValueError(f"cache head_dim {k_cache.shape[3]} != q head_dim {D}")
+    Hkv = k_cache.shape[2]
+    if Hkv == 0 or Hq % Hkv:
+        raise ValueError(f"num_q_heads={Hq} is not a multiple of num_kv_heads={Hkv}")
+    if block_table.shape[0] != B or seq_lens.numel() != B:
+        raise ValueError(f"batch mismatch: q {B}, block_table {block_table.shape[0]}, seq_lens {seq_lens.numel()}")
+    if out is not None:
         _check(out, "out", ndim=3)
-    if config is None:
-        config = default_decode_config(batch_size=q.shape[0], seq_len=int(max_seq_len), num_q_heads=q.shape[1],
-                                       num_kv_heads=k_cache.shape[2], head_dim=q.shape[2],
-                                       block_size=k_cache.shape[1], kv_dtype=_kv_name(k_cache))
-    var = decode_variant(config)
-    p = _decode_params(q, k_cache, v_cache, block_table, seq_lens, out, max_seq_len, softmax_scale,
-                       k_scale=k_scale, v_scale=v_scale)
-    nbytes = lib.b200attn_decode_workspace_size(p, var)
-    ws = _workspace(q.device, nbytes)
-    if ws is not None:
-        p.workspace = ws.data_ptr()
-        p.workspace_bytes = ws.numel()
-    _native.check(lib.b200attn_decode(p, var, torch.cuda.current_stream(q.device).cuda_stream))
-    return out
+        if out.shape != q.shape:
+            raise ValueError(f"out{tuple(out.shape)} must match q{tuple(q.shape)}")
+    _same_device(q, k_cache, v_cache, block_table, seq_lens, out)
 
 
 def decode_num_splits(q_shape, cache_shape, max_blocks_per_seq, max_seq_len, config: Mapping) -> int:
@@ -235,16 +292,43 @@ def cache_append(new_k: torch.Tensor, new_v: torch.Tensor, k_cache: torch.Tensor
     _check_cache(v_cache, "v_cache")
     _check(slot_mapping, "slot_mapping", dtype=torch.int64, ndim=1)
     NB, bs, Hkv, D = k_cache.shape
-    stream = torch.cuda.current_stream(new_k.device).cuda_stream
-    if _kv_dtype_code(k_cache) == _native.KV_FP8_E4M3:
-        if v_cache.dtype != FP8_DTYPE:
-            raise TypeError("k_cache / v_cache dtype mismatch")
-        _native.check(lib.b200attn_cache_append_fp8(_ptr(new_k), _ptr(new_v), _ptr(k_cache), _ptr(v_cache),
-                                                    _ptr(slot_mapping), new_k.shape[0], Hkv, D, bs, NB,
-                                                    float(k_scale or 1.0), float(v_scale or 1.0), stream))
-        return
-    _native.check(lib.b200attn_cache_append(_ptr(new_k), _ptr(new_v), _ptr(k_cache), _ptr(v_cache),
-                                            _ptr(slot_mapping), new_k.shape[0], Hkv, D, bs, NB, stream))
+    if k_cache.shape != v_cache.shape:
+        raise ValueError("k_cache / v_cache shape mismatch")
+    if new_k.shape != new_v.shape or new_k.shape[1:] != (Hkv, D):
+        raise ValueError(f"new_k{tuple(new_k.shape)} / new_v{tuple(new_v.shape)} must be [N, {Hkv}, {D}]")
+    if slot_mapping.numel() != new_k.shape[0]:
+        raise ValueError(f"slot_mapping has {slot_mapping.numel()} entries for {new_k.shape[0]} tokens")
+    _same_device(new_k, new_v, k_cache, v_cache, slot_mapping)
+    if k_cache.dtype != v_cache.dtype:
+        raise TypeError("k_cache / v_cache dtype mismatch")
+    with _on(new_k.device):
+        stream = torch.cuda.current_stream(new_k.device).cuda_stream
+        if _kv_dtype_code(k_cache) == _native.KV_FP8_E4M3:
+            _native.check(lib.b200attn_cache_append_fp8(_ptr(new_k), _ptr(new_v), _ptr(k_cache), _ptr(v_cache),
+                                                        _ptr(slot_mapping), new_k.shape[0], Hkv, D, bs, NB,
+                                                        float(k_scale or 1.0), float(v_scale or 1.0), stream))
+            return
+        _native.check(lib.b200attn_cache_append(_ptr(new_k), _ptr(new_v), _ptr(k_cache), _ptr(v_cache),
+                                                _ptr(slot_mapping), new_k.shape[0], Hkv, D, bs, NB, stream))
+
+
+class _NoGuard:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+_NO_GUARD = _NoGuard()
+
+
+def _on(device):
+    """Make `device` current for a launch (kernels go to the current device; the stream passed
+    belongs to `device`).  Free when it already is current — the common single-GPU case."""
+    if torch.cuda.current_device() == device.index:
+        return _NO_GUARD
+    return torch.cuda.device(device)
 
 
 def selftest_umma(mode: int, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
@@ -267,11 +351,7 @@ class DecodePlan:
     def __init__(self, q, k_cache, v_cache, block_table, seq_lens, out=None, max_seq_len=None, config=None,
                  softmax_scale=None, k_scale=None, v_scale=None):
         self.lib = _native.load()
-        _check(q, "q")
-        _check_cache(k_cache, "k_cache")
-        _check_cache(v_cache, "v_cache")
-        _check(block_table, "block_table", dtype=torch.int32, ndim=2)
-        _check(seq_lens, "seq_lens", dtype=torch.int32, ndim=1)
+        _check_decode_shapes(q, k_cache, v_cache, block_table, seq_lens, out)
         self.max_seq_len = int(max_seq_len if max_seq_len is not None else block_table.shape[1] * k_cache.shape[1])
         self.out = torch.empty_like(q) if out is None else out
         self.config = dict(config or default_decode_config(
@@ -291,22 +371,22 @@ class DecodePlan:
         return 2 if (self.num_splits > 1 or int(self.config["TILE_N"]) == 16) else 1
 
     def run(self, stream=None):
-        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
-        _native.check(self.lib.b200attn_decode(self.p, self.var, s))
+        with _on(self.device):
+            s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+            _native.check(self.lib.b200attn_decode(self.p, self.var, s))
         return self.out
 
     def run_partial(self, stream=None):
         """K2 only (the dominant kernel), for roofline timing."""
-        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
-        _native.check(self.lib.b200attn_decode_partial(self.p, self.var, s))
+        with _on(self.device):
+            s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+            _native.check(self.lib.b200attn_decode_partial(self.p, self.var, s))
 
 
 class PrefillPlan:
     def __init__(self, q, k, v, cu_seqlens, max_seqlen, out=None, causal=True, config=None, softmax_scale=None):
         self.lib = _native.load()
-        for t, n in ((q, "q"), (k, "k"), (v, "v")):
-            _check(t, n, ndim=3)
-        _check(cu_seqlens, "cu_seqlens", dtype=torch.int32, ndim=1)
+        _check_prefill_shapes(q, k, v, cu_seqlens, out)
         self.out = torch.empty_like(q) if out is None else out
         self.config = dict(config or default_prefill_config(
             num_seqs=cu_seqlens.numel() - 1, total_tokens=q.shape[0], max_seqlen=int(max_seqlen),
@@ -319,6 +399,7 @@ class PrefillPlan:
         self.device = q.device
 
     def run(self, stream=None):
-        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
-        _native.check(self.lib.b200attn_prefill(self.p, self.var, s))
+        with _on(self.device):
+            s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+            _native.check(self.lib.b200attn_prefill(self.p, self.var, s))
         return self.out

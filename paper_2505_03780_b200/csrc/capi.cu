@@ -13,7 +13,12 @@
 #include <cstring>
 #include <cstdlib>
 #include <algorithm>
+#include <atomic>
 #include <mutex>
+#include <set>
+#include <utility>
+
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges are free unless a profiler attaches
 
 #include "../../include/b200attn.h"
 #include "decode_flat_sm100.cuh"
@@ -22,6 +27,13 @@
 #include "selftest_sm100.cuh"
 
 namespace {
+
+// NVTX range around each host entry point (SURVEY §5 tracing): nsys / ncu --nvtx see which API call
+// enqueued which kernels
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 constexpr int kMaxSmem = 232448;  // 227 KB opt-in per CTA on sm_100a
 constexpr int kNumSMs = 148;
@@ -97,6 +109,28 @@ int make_map_u8_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, u
   return B200ATTN_OK;
 }
 
+// Function attributes (the >48-KB dynamic smem opt-in) live in each device's context: track them
+// per (kernel, device) so a process that launches on several GPUs sets them on every one.
+// Thread-safe; the lock is held only for the set lookup (the attribute call happens once).
+constexpr int kMaxDevices = 64;
+
+int ensure_smem_attr(const void* kern, int bytes, const char* what) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count({kern, dev})) return B200ATTN_OK;
+  }
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  std::lock_guard<std::mutex> g(mu);
+  done.insert({kern, dev});
+  return B200ATTN_OK;
+}
+
 int num_sms();
 
 // ------------------------------------------------------------------ prefill variants
@@ -127,12 +161,9 @@ template <int NQ, int BN, int NS, int SPLIT>
 int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   using C = b200::PrefillCfg<NQ, BN, NS, SPLIT>;
   auto kern = b200::prefill_fwd_kernel<NQ, BN, NS, kPrefillEmu, SPLIT>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(prefill)");
-    attr_done = true;
-  }
+  if (int rc0 = ensure_smem_attr(reinterpret_cast<const void*>(kern), C::SMEM_BYTES,
+                               "cudaFuncSetAttribute(prefill)"))
+    return rc0;
   const int D = 128;
   CUtensorMap mq, mk, mv;
   int rc;
@@ -261,12 +292,9 @@ template <int NS>
 int launch_decode(const b200attn_decode_params* p, int splits, int tps, bool combine, cudaStream_t stream) {
   using C = b200::DecodeCfg<NS>;
   auto kern = b200::decode_split_kernel<NS>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode)");
-    attr_done = true;
-  }
+  if (int rc0 = ensure_smem_attr(reinterpret_cast<const void*>(kern), C::SMEM_BYTES,
+                               "cudaFuncSetAttribute(decode)"))
+    return rc0;
   const int D = 128, G = p->num_q_heads / p->num_kv_heads;
   CUtensorMap mq, mk, mv;
   int rc;
@@ -319,12 +347,15 @@ const DecodeEntry kDecode[] = {DF(2), DF(3), DF(4), DF(5), DF(6)};
 
 
 // ---- K2' flat partition (TILE_N = 16: one page of all 8 kv heads per MMA tile)
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+int num_sms() {  // per device (cached; a process may drive several GPUs)
+  static std::atomic<int> cache[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return kNumSMs;
+  std::atomic<int>& c = cache[dev & (kMaxDevices - 1)];
+  int n = c.load(std::memory_order_relaxed);
+  if (n <= 0) {
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
+    c.store(n, std::memory_order_relaxed);
   }
   return n;
 }
@@ -342,12 +373,9 @@ template <int G, int NS, bool FP8>
 int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stream) {
   using C = b200::FlatCfg<G, NS, FP8>;
   auto kern = b200::decode_flat_kernel<G, NS, FP8>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode_flat)");
-    attr_done = true;
-  }
+  if (int rc0 = ensure_smem_attr(reinterpret_cast<const void*>(kern), C::SMEM_BYTES,
+                               "cudaFuncSetAttribute(decode_flat)"))
+    return rc0;
   const int D = 128;
   CUtensorMap mq, mk, mv;
   int rc;
@@ -574,6 +602,7 @@ size_t b200attn_prefill_workspace_size(const b200attn_prefill_params* p) {
 }
 
 int b200attn_prefill(const b200attn_prefill_params* p, const b200attn_prefill_variant* v, void* stream) {
+  NvtxRange nvtx("b200attn_prefill");
   const PrefillEntry* e;
   g_err[0] = 0;
   int rc = check_prefill(p, v, &e);
@@ -617,6 +646,7 @@ size_t b200attn_decode_workspace_size(const b200attn_decode_params* p, const b20
 
 static int decode_impl(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream,
                        bool combine) {
+  NvtxRange nvtx("b200attn_decode");
   DecodeChoice c;
   g_err[0] = 0;
   int rc = resolve_decode(p, v, &c);
@@ -660,6 +690,7 @@ int b200attn_combine(const float* part_o, const float* part_ml, void* o, int32_t
 int b200attn_cache_append(const void* new_k, const void* new_v, void* k_cache, void* v_cache,
                           const int64_t* slot_mapping, int32_t num_tokens, int32_t num_kv_heads, int32_t head_dim,
                           int32_t block_size, int32_t num_blocks, void* stream) {
+  NvtxRange nvtx("b200attn_cache_append");
   g_err[0] = 0;
   if (head_dim != 128) return fail(B200ATTN_UNSUPPORTED_CONFIG, "head_dim=%d (compiled for 128)", head_dim);
   if (!new_k || !new_v || !k_cache || !v_cache || !slot_mapping || num_tokens < 0 || num_kv_heads <= 0)
@@ -679,6 +710,7 @@ int b200attn_cache_append(const void* new_k, const void* new_v, void* k_cache, v
 int b200attn_cache_append_fp8(const void* new_k, const void* new_v, void* k_cache, void* v_cache,
                               const int64_t* slot_mapping, int32_t num_tokens, int32_t num_kv_heads, int32_t head_dim,
                               int32_t block_size, int32_t num_blocks, float k_scale, float v_scale, void* stream) {
+  NvtxRange nvtx("b200attn_cache_append_fp8");
   g_err[0] = 0;
   if (head_dim != 128) return fail(B200ATTN_UNSUPPORTED_CONFIG, "head_dim=%d (compiled for 128)", head_dim);
   if (!new_k || !new_v || !k_cache || !v_cache || !slot_mapping || num_tokens < 0 || num_kv_heads <= 0)

@@ -164,9 +164,9 @@ __device__ __forceinline__ void prefill_decode_item(int w, const PrefillKernelAr
     qblk = a.single_nqb - 1 - pair;
     return;
   }
-  const int it = a.items[pair];
-  seq = it >> 16;
-  qblk = it & 0xFFFF;
+  const uint32_t it = static_cast<uint32_t>(a.items[pair]);  // (seq << 16) | q block, seq < 65536
+  seq = static_cast<int>(it >> 16);
+  qblk = static_cast<int>(it & 0xFFFFu);
 }
 
 // Pass 2 over one S row: P = exp2(S*sl2 - m) -> bf16 pairs written back over the S columns;
@@ -723,12 +723,14 @@ __global__ void __launch_bounds__(1024) prefill_schedule_kernel(const int32_t* _
   for (int s = warp; s < num_seqs; s += 32) {
     const int nqb = (cu[s + 1] - cu[s] + 127) / 128;
     if (causal) {
-      for (int qb = lane; qb < nqb; qb += 32) items[atomicAdd(&hist[qb], 1)] = (s << 16) | qb;
+      for (int qb = lane; qb < nqb; qb += 32)
+        items[atomicAdd(&hist[qb], 1)] = static_cast<int32_t>((static_cast<uint32_t>(s) << 16) | qb);
     } else if (nqb > 0) {
       int base = 0;
       if (lane == 0) base = atomicAdd(&hist[nqb - 1], nqb);
       base = __shfl_sync(0xffffffffu, base, 0);
-      for (int qb = lane; qb < nqb; qb += 32) items[base + qb] = (s << 16) | qb;
+      for (int qb = lane; qb < nqb; qb += 32)
+        items[base + qb] = static_cast<int32_t>((static_cast<uint32_t>(s) << 16) | qb);
     }
   }
   if (tid == 0) {

@@ -13,6 +13,7 @@ from __future__ import annotations
 import json
 import math
 import os
+from collections import OrderedDict
 from pathlib import Path
 from typing import Optional
 
@@ -76,17 +77,37 @@ def reset():
     _lookup_cache.clear()
 
 
-_lookup_cache: dict = {}
+_lookup_cache: "OrderedDict" = OrderedDict()
+_LOOKUP_MAX = 4096  # LRU bound (a serving loop's token counts change every step)
+_BUCKETED = ("batch_size", "seq_len", "total_tokens", "max_seqlen")
+
+
+def _memo_key(op: str, dims: dict):
+    """Geometry exact, sizes bucketed to quarter-octaves (the lookup's own distance is a log2 sum),
+    so a serving loop whose total_tokens / max_seqlen drift every step still hits the memo."""
+    items = []
+    for k, v in sorted(dims.items()):
+        if k in _BUCKETED and isinstance(v, (int, float)) and v > 0:
+            v = ("b", round(4 * math.log2(v)))
+        items.append((k, v))
+    return op, tuple(items)
 
 
 def lookup(op: str, dims: dict) -> Optional[dict]:
-    """Nearest tuned config (memoised per (op, dims): a serving loop asks the same shape every step)."""
-    key = (op, tuple(sorted(dims.items())))
-    if key in _lookup_cache:
-        return _lookup_cache[key]
+    """Nearest tuned config, memoised per bucketed shape (LRU-bounded)."""
+    key = _memo_key(op, dims)
+    cfg = _lookup_cache.get(key, _MISS)
+    if cfg is not _MISS:
+        _lookup_cache.move_to_end(key)
+        return cfg
     cfg = _lookup(op, dims)
     _lookup_cache[key] = cfg
+    if len(_lookup_cache) > _LOOKUP_MAX:
+        _lookup_cache.popitem(last=False)
     return cfg
+
+
+_MISS = object()
 
 
 def _lookup(op: str, dims: dict) -> Optional[dict]:

@@ -1,0 +1,48 @@
+#!/usr/bin/env bash
+# One parameterised gpurun job runner (replaces round 1's one-shot scripts/jobs/gpu_r1s*.sh).
+#   gpurun --timeout T -- 'bash scripts/gpujob.sh TAG recipe [recipe ...]'
+# Each recipe writes gpurun_out/TAG_<recipe>.* ; every step has its own timeout so a hang is cut
+# short before gpurun's limit.  Recipes:
+#   tests      pytest -m gpu (+ per-config parity table)       smoke     __graft_entry__.smoke()
+#   bench      default bench line                               benchref  bench.py --impl reference
+#   benchpf    bench.py --workload prefill                      c4        bench.py --workload c4 (full C4 on 1 GPU)
+#   dist2      2 ranks on one GPU (gloo) through bench.py's N>1 path, with the gather + oracle check
+#   launches   ncu launch lists (gpu__time_duration) of the decode and prefill bench workloads
+#   ncupf      ncu --set full of K1 on C3                       ncudec    ncu --set full of K2' on C2
+#   sanitize   compute-sanitizer memcheck/racecheck/synccheck on small cases of every kernel
+#   sota       scripts/sota.py (same-box library comparators)   single    single-launch vs amortised
+#   perf       scripts/perf.py time over the BASELINE shapes
+set -u
+TAG=$1; shift
+mkdir -p gpurun_out
+export PYTHONPATH=$PWD
+O=gpurun_out/$TAG
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,temperature.gpu --format=csv > ${O}_smi.txt 2>&1
+for r in "$@"; do
+  echo "== $r" >&2
+  case $r in
+    tests) timeout 1500 python -m pytest tests -m gpu -x -q -rs > ${O}_tests.log 2>&1; tail -40 ${O}_tests.log ;;
+    smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > ${O}_smoke.log 2>&1; tail -3 ${O}_smoke.log ;;
+    bench) timeout 900 python bench.py --steps 20 --warmup 5 > ${O}_bench.json 2> ${O}_bench.err; cat ${O}_bench.json; tail -5 ${O}_bench.err ;;
+    benchref) timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > ${O}_benchref.json 2>&1; cat ${O}_benchref.json ;;
+    benchpf) timeout 900 python bench.py --workload prefill --steps 50 --warmup 5 --no-cpu-baseline > ${O}_benchpf.json 2>&1; cat ${O}_benchpf.json ;;
+    c4) timeout 1200 python bench.py --workload c4 --steps 10 --warmup 3 --no-cpu-baseline > ${O}_c4.json 2>&1; cat ${O}_c4.json ;;
+    dist2) B200_BENCH_ALLOW_SHARED_GPU=1 timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+             --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --steps 5 --warmup 3 --no-cpu-baseline \
+             --dist-backend gloo > ${O}_dist2.json 2> ${O}_dist2.err; cat ${O}_dist2.json; tail -20 ${O}_dist2.err ;;
+    launches)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${O}_launches_decode.csv \
+        python bench.py --steps 3 --warmup 3 --no-extra --no-cpu-baseline > /dev/null 2>&1
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${O}_launches_prefill.csv \
+        python bench.py --workload prefill --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 ;;
+    ncupf) timeout 900 ncu --set full --clock-control none --import-source on -k regex:prefill_fwd -s 2 -c 1 \
+             -o ${O}_pf python scripts/perf.py prof --op prefill > ${O}_ncupf.log 2>&1; tail -3 ${O}_ncupf.log ;;
+    ncudec) timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_flat -s 2 -c 1 \
+             -o ${O}_dec python scripts/perf.py prof --op decode > ${O}_ncudec.log 2>&1; tail -3 ${O}_ncudec.log ;;
+    sanitize) timeout 2400 bash scripts/sanitize.sh ${O}_sanitize ;;
+    sota) timeout 2400 python scripts/sota.py --out ${O}_sota.json > ${O}_sota.log 2>&1; tail -30 ${O}_sota.log ;;
+    single) timeout 600 python scripts/perf.py single --shapes C3,C1 > ${O}_single.log 2>&1; cat ${O}_single.log ;;
+    perf) timeout 900 python scripts/perf.py time --shapes C1,C3,1x16k,C2,C4shard,C2fp8 > ${O}_perf.log 2>&1; cat ${O}_perf.log ;;
+    *) echo "unknown recipe $r" >&2 ;;
+  esac
+done

@@ -1,0 +1,185 @@
+#!/usr/bin/env python
+"""Device-time probes of the kernels (one tool instead of round 1's per-experiment scripts).
+
+  perf.py time    --op prefill|decode --shapes C1,C3,1x16k --cfg '{json}' | --all-variants [--reps N]
+      graph-replayed per-launch time (N launches per replay) and TFLOP/s or GB/s
+  perf.py single  --op prefill --shapes C3  -- one launch per event pair after an idle gap (cold clocks)
+  perf.py prof    --op prefill|decode|c1 [--cfg json] [--n 3]   -- small driver for ncu / sanitizers
+  perf.py trace   [BLOCK_M num_stages num_warps]                 -- clock64 trace (needs a -DB200_TRACE build)
+  perf.py umma-rate                                              -- tcgen05 MMA issue-rate probe
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import statistics
+import sys
+import time
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from paper_2505_03780_b200 import _native  # noqa: E402
+from paper_2505_03780_b200 import attention as A  # noqa: E402
+from paper_2505_03780_b200 import workload as W  # noqa: E402
+
+SHAPES = {
+    "C1": ("prefill", W.C1), "C3": ("prefill", W.C3), "1x16k": ("prefill", dict(W.C1, seq_len=16384)),
+    "4x8k": ("prefill", dict(W.C1, batch_size=4, seq_len=8192)),
+    "C2": ("decode", W.C2), "C4shard": ("decode", dict(W.C4, batch_size=32)),
+    "C2fp8": ("decode", dict(W.C2, kv_dtype="fp8_e4m3")), "b1x32k": ("decode", dict(W.C2, batch_size=1, seq_len=32768)),
+}
+
+
+def make_plan(op, shape, cfg):
+    if op == "prefill":
+        x = W.make_prefill(shape, device="cuda")
+        return A.PrefillPlan(x.q, x.k, x.v, x.cu_seqlens, x.max_seqlen, config=cfg), x.flops, 1e12, "TFLOP/s"
+    d = W.make_decode(shape, device="cuda")
+    p = A.DecodePlan(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens, max_seq_len=d.max_seq_len, config=cfg,
+                     k_scale=d.k_scale, v_scale=d.v_scale)
+    return p, d.total_bytes, 1e9, "GB/s"
+
+
+def graph_ms(fn, reps):
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    out = []
+    for _ in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        g.replay()
+        e.record()
+        torch.cuda.synchronize()
+        out.append(s.elapsed_time(e) / reps)
+    return statistics.median(out)
+
+
+def all_prefill_variants():
+    for bm in (256, 128):
+        for bn in (128, 64):
+            for ns in (1, 2, 3, 4):
+                yield dict(BLOCK_M=bm, BLOCK_N=bn, num_warps=4, num_stages=ns, waves_per_eu=1, PRE_LOAD_V=False)
+        for ns in (1, 2):
+            yield dict(BLOCK_M=bm, BLOCK_N=128, num_warps=8, num_stages=ns, waves_per_eu=1, PRE_LOAD_V=False)
+
+
+def cmd_time(a):
+    for name in a.shapes.split(","):
+        op, shape = SHAPES[name]
+        cfgs = [json.loads(a.cfg) if a.cfg else None]
+        if a.all_variants and op == "prefill":
+            cfgs = list(all_prefill_variants())
+        for cfg in cfgs:
+            try:
+                p, work, sc, unit = make_plan(op, shape, cfg)
+                reps = a.reps or (200 if name == "C1" else 10)
+                ms = graph_ms(p.run, reps)
+                print(json.dumps({"tag": a.tag, "shape": name, "cfg": p.config, "us": ms * 1e3,
+                                  unit: work / (ms / 1e3) / sc}), flush=True)
+                del p
+            except Exception as ex:
+                print(json.dumps({"tag": a.tag, "shape": name, "cfg": cfg, "error": str(ex)[:200]}), flush=True)
+            torch.cuda.empty_cache()
+
+
+def cmd_single(a):
+    """single launches separated by idle gaps (what a protocol-median evaluation sees) vs back-to-back."""
+    for name in a.shapes.split(","):
+        op, shape = SHAPES[name]
+        p, work, sc, unit = make_plan(op, shape, json.loads(a.cfg) if a.cfg else None)
+        p.run()
+        torch.cuda.synchronize()
+        res = {}
+        for gap in (0.0, 0.002, 0.05):
+            ts = []
+            for _ in range(10):
+                if gap:
+                    time.sleep(gap)
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                p.run()
+                e.record()
+                torch.cuda.synchronize()
+                ts.append(s.elapsed_time(e))
+            res[f"gap_{gap}s_us"] = statistics.median(ts) * 1e3
+        res["graph_amortised_us"] = graph_ms(p.run, 10) * 1e3
+        print(json.dumps({"tag": a.tag, "shape": name, **res}), flush=True)
+
+
+def cmd_prof(a):
+    cfg = json.loads(a.cfg) if a.cfg else None
+    op, shape = {"decode": SHAPES["C2"], "prefill": SHAPES["C3"], "c1": SHAPES["C1"]}.get(a.op, SHAPES.get(a.op))
+    p, *_ = make_plan(op, shape, cfg)
+    for _ in range(a.n):
+        p.run()
+    torch.cuda.synchronize()
+    print("done")
+
+
+def cmd_trace(a):
+    lib = _native.load()
+    cfg = None
+    if len(a.args) >= 3:
+        bm, ns, nw = map(int, a.args[:3])
+        cfg = dict(BLOCK_M=bm, BLOCK_N=128, num_warps=nw, num_stages=ns, waves_per_eu=1, PRE_LOAD_V=False)
+    import numpy as np
+
+    x = W.make_prefill(dict(W.C1, batch_size=4, seq_len=8192), device="cuda")
+    p = A.PrefillPlan(x.q, x.k, x.v, x.cu_seqlens, x.max_seqlen, config=cfg)
+    for _ in range(3):
+        p.run()
+    torch.cuda.synchronize()
+    buf = (ctypes.c_ulonglong * (16 * 512))()
+    lib.b200attn_debug_trace(buf, 16 * 512)
+    t = np.frombuffer(buf, dtype=np.uint64).reshape(16, 512).astype(np.int64)
+    rows = [np.concatenate([t[:, j] - t[0, j], [t[0, j] - t[0, j - 1]]]) for j in range(1, 40)]
+    print("config", cfg)
+    print("median cycles rel. to S0 of each step:", " ".join(f"{v:.0f}" for v in np.median(np.array(rows[5:]), 0)))
+
+
+def cmd_umma_rate(a):
+    lib = _native.load()
+    out = torch.zeros(148, dtype=torch.int64, device="cuda")
+    modes = [(0, "SS N128 B-K (QK)", 128), (1, "TS N128 B-MN (PV, P in TMEM)", 128), (2, "SS N128 B-MN", 128),
+             (3, "SS N256 B-K", 256), (4, "TS N128 B-K", 128), (5, "SS N64 B-K", 64), (6, "SS N256 B-MN", 256),
+             (7, "TS N64 B-MN", 64), (8, "SS N128 B-K + 4 LDTM/STTM warps", 128),
+             (9, "TS N128 B-MN + 4 LDTM/STTM warps", 128), (10, "SS N128 B-K + 8 LDTM/STTM warps", 128)]
+    for mode, name, N in modes:
+        rc = lib.b200attn_debug_umma_rate(mode, 4000, 148, ctypes.c_void_p(out.data_ptr()),
+                                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        assert rc == 0, lib.b200attn_last_error()
+        cyc = out.float().mean().item()
+        ideal = N * 128 / 256 * 8
+        print(f"{name:34s}: {cyc:7.1f} cycles / 8 MMAs (floor {ideal:.0f}) -> {ideal / cyc * 100:.0f}% of floor")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cmd", choices=["time", "single", "prof", "trace", "umma-rate"])
+    ap.add_argument("args", nargs="*")
+    ap.add_argument("--op", default="prefill")
+    ap.add_argument("--shapes", default="C3")
+    ap.add_argument("--cfg", default=None)
+    ap.add_argument("--all-variants", action="store_true")
+    ap.add_argument("--reps", type=int, default=0)
+    ap.add_argument("--n", type=int, default=3)
+    ap.add_argument("--tag", default="")
+    a = ap.parse_args()
+    {"time": cmd_time, "single": cmd_single, "prof": cmd_prof, "trace": cmd_trace, "umma-rate": cmd_umma_rate}[a.cmd](a)
+
+
+if __name__ == "__main__":
+    main()

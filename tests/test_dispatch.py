@@ -61,3 +61,15 @@ def test_shipped_table_covers_the_baseline_configs():
     assert len(rows["prefill"]) >= 78 and len(rows["decode"]) >= 81
     c2 = D.default_decode_config(batch_size=64, seq_len=4096, block_size=16, **HEADS)
     assert c2["TILE_N"] == 16
+
+
+def test_lookup_memo_is_bucketed_and_bounded(table, monkeypatch):
+    """A serving loop's drifting token counts must neither grow the memo per step nor miss it."""
+    D._lookup_cache.clear()
+    for t in range(20000, 20400):  # 400 distinct total_tokens within one quarter-octave bucket
+        D.default_prefill_config(num_seqs=16, total_tokens=t, max_seqlen=2048, causal=True, **HEADS)
+    assert len(D._lookup_cache) <= 2
+    monkeypatch.setattr(D, "_LOOKUP_MAX", 8)
+    for b in range(1, 200):
+        D.default_decode_config(batch_size=b * 7, seq_len=4096, block_size=16, **HEADS)
+    assert len(D._lookup_cache) <= 8
