@@ -129,6 +129,38 @@ def prefill_np(q, k, v, cu_seqlens, causal=True, scale=None):
     return out
 
 
+def prefill_blas(q, k, v, cu_seqlens, causal=True, scale=None, heads=None, chunk=1024):
+    """Same semantics as ``prefill`` in fp64 through BLAS matmuls (torch fp64 on the host cores:
+    multithreaded matmuls AND elementwise passes), chunked over query rows so a causal chunk only
+    touches keys up to its last row: the full-size parity tests (all of C3's 16 sequences x 32
+    heads) finish in seconds instead of minutes.  ``heads`` restricts the work (and the output)
+    to those q heads.  Returns fp64 numpy [T, len(heads), D]."""
+    import torch
+
+    qf, kf, vf = (torch.from_numpy(bf16_bits_to_f64(as_bf16_bits(x))) for x in (q, k, v))
+    cu = _i32(cu_seqlens)
+    T, Hq, D = qf.shape
+    G = Hq // kf.shape[1]
+    heads = list(range(Hq)) if heads is None else list(heads)
+    scale = float(scale) if scale else 1.0 / np.sqrt(D)
+    out = torch.zeros((T, len(heads), D), dtype=torch.float64)
+    for s in range(len(cu) - 1):
+        a, b = int(cu[s]), int(cu[s + 1])
+        for hi, h in enumerate(heads):
+            kk, vv = kf[a:b, h // G], vf[a:b, h // G]  # [L, D]
+            for r0 in range(0, b - a, chunk):
+                r1 = min(b - a, r0 + chunk)
+                kend = r1 if causal else b - a
+                sc = (qf[a + r0:a + r1, h] @ kk[:kend].T) * scale  # [rows, kend]
+                if causal:
+                    mask = torch.arange(kend)[None, :] > torch.arange(r0, r1)[:, None]
+                    sc.masked_fill_(mask, -float("inf"))
+                sc -= sc.amax(-1, keepdim=True)
+                sc.exp_()
+                out[a + r0:a + r1, hi] = (sc @ vv[:kend]) / sc.sum(-1, keepdim=True)
+    return out.numpy()
+
+
 def decode_np(q, k_cache, v_cache, block_table, seq_lens, scale=None):
     qf = bf16_bits_to_f64(as_bf16_bits(q))
     kc, vc = (bf16_bits_to_f64(as_bf16_bits(x)) for x in (k_cache, v_cache))

@@ -403,3 +403,86 @@ class PrefillPlan:
             s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
             _native.check(self.lib.b200attn_prefill(self.p, self.var, s))
         return self.out
+
+
+def pack_pinned(tensors, align: int = 256):
+    """Copy host tensors into one pinned byte buffer; returns (buffer, [(offset, shape, dtype)])."""
+    offs, n = [], 0
+    for t in tensors:
+        n = (n + align - 1) // align * align
+        offs.append(n)
+        n += t.numel() * t.element_size()
+    buf = torch.empty(max(n, 1), dtype=torch.uint8).pin_memory()
+    views = []
+    for t, o in zip(tensors, offs):
+        nb = t.numel() * t.element_size()
+        buf[o:o + nb].copy_(t.contiguous().view(-1).view(torch.uint8))
+        views.append((o, tuple(t.shape), t.dtype))
+    return buf, views
+
+
+def unpack_view(buf: torch.Tensor, v) -> torch.Tensor:
+    o, shape, dtype = v
+    nb = math.prod(shape) * torch.empty(0, dtype=dtype).element_size()
+    return buf[o:o + nb].view(dtype).view(shape)
+
+
+class DecodeStep:
+    """One serving decode step as ONE CUDA graph, host buffers in and out:
+
+        H2D (pinned staging: q, the new token's K/V, slot_mapping, seq_lens)
+        -> cache_append (new K/V into its page slot) -> paged_decode -> D2H (output, pinned)
+
+    The caller writes this step's inputs into ``q_host`` / ``new_k_host`` / ``new_v_host`` /
+    ``slots_host`` / ``seq_lens_host`` and calls the object; ``out_host`` holds the result once the
+    stream reaches the end of the step (``sync=True`` waits for it).  The paged KV pool and the
+    block table stay resident on the device: a serving loop appends one page index per sequence
+    every ``block_size`` steps, in place.  One graph replay = 1 memcpy + 2-3 kernels + 1 memcpy,
+    no per-call host work beyond the replay itself."""
+
+    def __init__(self, k_cache, v_cache, block_table, batch: int, num_q_heads: int, max_seq_len=None, config=None,
+                 softmax_scale=None, k_scale=None, v_scale=None):
+        dev = k_cache.device
+        _check_cache(k_cache, "k_cache")
+        Hkv, D = k_cache.shape[2], k_cache.shape[3]
+        B, Hq = int(batch), int(num_q_heads)
+        proto = (torch.empty(B, Hq, D, dtype=torch.bfloat16), torch.empty(B, Hkv, D, dtype=torch.bfloat16),
+                 torch.empty(B, Hkv, D, dtype=torch.bfloat16), torch.full((B,), -1, dtype=torch.int64),
+                 torch.zeros(B, dtype=torch.int32))
+        self.stage_h, views = pack_pinned(proto)
+        self.q_host, self.new_k_host, self.new_v_host, self.slots_host, self.seq_lens_host = (
+            unpack_view(self.stage_h, v) for v in views)
+        self.stage_d = torch.empty_like(self.stage_h, device=dev)
+        q_d, nk_d, nv_d, slots_d, sl_d = (unpack_view(self.stage_d, v) for v in views)
+        self.out_host = torch.empty(B, Hq, D, dtype=torch.bfloat16).pin_memory()
+        self.h2d_bytes = self.stage_h.numel()
+        self.d2h_bytes = self.out_host.numel() * 2
+        self.plan = DecodePlan(q_d, k_cache, v_cache, block_table, sl_d, max_seq_len=max_seq_len, config=config,
+                               softmax_scale=softmax_scale, k_scale=k_scale, v_scale=v_scale)
+        self.device = dev
+
+        def body():
+            self.stage_d.copy_(self.stage_h, non_blocking=True)
+            cache_append(nk_d, nv_d, k_cache, v_cache, slots_d, k_scale=k_scale, v_scale=v_scale)
+            self.plan.run()
+            self.out_host.copy_(self.plan.out, non_blocking=True)
+
+        with _on(dev):
+            s = torch.cuda.Stream(dev)
+            s.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(s):
+                body()  # warm: attributes, descriptor prefetch (slots are -1: nothing written)
+            torch.cuda.current_stream(dev).wait_stream(s)
+            torch.cuda.synchronize(dev)
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                body()
+        self.done = torch.cuda.Event()
+
+    def __call__(self, sync: bool = False) -> torch.Tensor:
+        with _on(self.device):
+            self.graph.replay()
+            if sync:
+                self.done.record()
+                self.done.synchronize()
+        return self.out_host

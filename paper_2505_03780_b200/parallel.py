@@ -60,8 +60,9 @@ def gather_to_rank0(t: torch.Tensor, counts: list[int]):
         return t
     world, rank = dist.get_world_size(), dist.get_rank()
     pad = max(counts)
-    buf = torch.zeros((pad,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-    buf[: t.shape[0]] = t
+    dev = t.device if dist.get_backend() == "nccl" else torch.device("cpu")  # gloo gathers host tensors
+    buf = torch.zeros((pad,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+    buf[: t.shape[0]] = t.to(dev)
     bufs = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
     dist.gather(buf, bufs, dst=0)
     if rank != 0:

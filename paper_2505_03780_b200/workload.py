@@ -151,3 +151,80 @@ C3 = {"op": "prefill", "batch_size": 16, "seq_len_min": 128, "seq_len_max": 8192
       "num_q_heads": 32, "num_kv_heads": 8, "head_dim": 128, "causal": True, "dtype": "bfloat16", "seed": 0}
 C4 = {"op": "decode", "batch_size": 256, "seq_len": 32768, "num_q_heads": 64, "num_kv_heads": 8, "head_dim": 128,
       "block_size": 16, "dtype": "bfloat16", "seed": 0}
+
+
+# ----------------------------------------------------------------------------- sharded workloads
+# Multi-GPU: the path shards with no exchange step, so each rank builds ONLY its
+# shard.  Content is a function of the global unit (sequence for decode, kv head for prefill), never
+# of the sharding, so any rank — rank 0 validating a gathered result — can rebuild any unit.
+_SEQ_STRIDE = 1_000_003
+
+
+def _unit_randn(shape, seed: int, unit: int, salt: int, device, fp8: bool = False) -> torch.Tensor:
+    g = torch.Generator(device=device).manual_seed(seed * _SEQ_STRIDE + unit * 8 + salt)
+    x = torch.randn(shape, generator=g, dtype=torch.float32, device=device)
+    return (x * FP8_INV_SCALE).to(torch.float8_e4m3fn) if fp8 else x.to(torch.bfloat16)
+
+
+def decode_sequence(shape: dict, b: int, device="cuda"):
+    """q [Hq, D], k/v [ctx, Hkv, D] of global sequence b of a sharded decode workload."""
+    seed = int(shape.get("seed", 0))
+    ctx, Hq, Hkv, D = (int(shape[k]) for k in ("seq_len", "num_q_heads", "num_kv_heads", "head_dim"))
+    fp8 = str(shape.get("kv_dtype", "bfloat16")).startswith(("fp8", "float8"))
+    q = _unit_randn((Hq, D), seed, b, 0, device)
+    k = _unit_randn((ctx, Hkv, D), seed, b, 1, device, fp8)
+    v = _unit_randn((ctx, Hkv, D), seed, b, 2, device, fp8)
+    return q, k, v
+
+
+def make_decode_shard(shape: dict, start: int, count: int, device="cuda") -> DecodeInputs:
+    """Sequences [start, start + count) of the decode workload `shape` (every one seq_len long),
+    paged into a pool holding only this shard's pages, block table permuted (seeded by start)."""
+    ctx, Hq, Hkv, D = (int(shape[k]) for k in ("seq_len", "num_q_heads", "num_kv_heads", "head_dim"))
+    bs = int(shape.get("block_size", 16))
+    nblk = (ctx + bs - 1) // bs
+    fp8 = str(shape.get("kv_dtype", "bfloat16")).startswith(("fp8", "float8"))
+    dt = torch.float8_e4m3fn if fp8 else torch.bfloat16
+    NB = max(1, count * nblk)
+    kc = torch.zeros((NB, bs, Hkv, D), dtype=dt, device=device)
+    vc = torch.zeros_like(kc)
+    q = torch.empty((count, Hq, D), dtype=torch.bfloat16, device=device)
+    g = torch.Generator(device="cpu").manual_seed(int(shape.get("seed", 0)) * _SEQ_STRIDE + start)
+    perm = torch.randperm(NB, generator=g).to(torch.int32)
+    bt = perm[: count * nblk].reshape(count, nblk).to(device)
+    pad = nblk * bs - ctx
+    for i in range(count):
+        qi, ki, vi = decode_sequence(shape, start + i, device)
+        q[i] = qi
+        rows = bt[i].long()
+        if pad:
+            ki = torch.cat([ki, torch.zeros((pad, Hkv, D), dtype=dt, device=device)])
+            vi = torch.cat([vi, torch.zeros((pad, Hkv, D), dtype=dt, device=device)])
+        kc[rows] = ki.view(nblk, bs, Hkv, D)
+        vc[rows] = vi.view(nblk, bs, Hkv, D)
+    sc = 1.0 / FP8_INV_SCALE if fp8 else None
+    return DecodeInputs(q, kc, vc, bt, torch.full((count,), ctx, dtype=torch.int32, device=device), ctx,
+                        [ctx] * count, sc, sc)
+
+
+def prefill_kv_head(shape: dict, kvh: int, device="cuda"):
+    """q [T, G, D] (the G q heads of kv head kvh), k/v [T, 1, D] of a head-sharded prefill workload."""
+    seed = int(shape.get("seed", 0))
+    T = sum(varlen_lengths(shape))
+    Hq, Hkv, D = int(shape["num_q_heads"]), int(shape["num_kv_heads"]), int(shape["head_dim"])
+    G = Hq // Hkv
+    return (_unit_randn((T, G, D), seed, kvh, 3, device), _unit_randn((T, 1, D), seed, kvh, 4, device),
+            _unit_randn((T, 1, D), seed, kvh, 5, device))
+
+
+def make_prefill_heads(shape: dict, kv_heads: range, device="cuda") -> PrefillInputs:
+    """kv heads `kv_heads` (and their q heads) of the prefill workload `shape`: the head shard a
+    rank owns when prefill is split by GQA group."""
+    lens = varlen_lengths(shape)
+    parts = [prefill_kv_head(shape, h, device) for h in kv_heads]
+    q = torch.cat([p[0] for p in parts], 1).contiguous()
+    k = torch.cat([p[1] for p in parts], 1).contiguous()
+    v = torch.cat([p[2] for p in parts], 1).contiguous()
+    cu = torch.zeros(len(lens) + 1, dtype=torch.int32)
+    cu[1:] = torch.cumsum(torch.tensor(lens, dtype=torch.int32), 0)
+    return PrefillInputs(q, k, v, cu.to(device), max(lens), lens, bool(shape.get("causal", True)))

@@ -1,0 +1,138 @@
+"""GPU tests of the public API's host-side contract: cross-shape validation, per-stream workspaces
+(reentrancy), the one-graph serving step, and the multi-rank bench path (2 ranks: NCCL on two GPUs,
+or gloo with both ranks on one GPU when only one is visible)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2505_03780_b200 import attention as A
+from paper_2505_03780_b200 import workload as W
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+DEV = "cuda"
+
+
+def test_decode_rejects_mismatched_shapes():
+    d = W.make_decode(dict(W.C2, batch_size=4, seq_len=64), device=DEV)
+    with pytest.raises(ValueError, match="batch mismatch"):
+        A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table[:3], d.seq_lens)
+    with pytest.raises(ValueError, match="batch mismatch"):
+        A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens[:2])
+    with pytest.raises(ValueError, match="out"):
+        A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens, out=torch.empty_like(d.q[:2]))
+    with pytest.raises(ValueError, match="head_dim"):
+        A.paged_decode(d.q[..., :64].contiguous(), d.k_cache, d.v_cache, d.block_table, d.seq_lens)
+    with pytest.raises(ValueError, match="multiple"):
+        A.paged_decode(d.q[:, :12].contiguous(), d.k_cache, d.v_cache, d.block_table, d.seq_lens)
+
+
+def test_prefill_and_append_reject_mismatched_shapes():
+    x = W.make_prefill(dict(W.C1, seq_len=64), device=DEV)
+    with pytest.raises(ValueError):
+        A.prefill_varlen(x.q, x.k[:10], x.v[:10], x.cu_seqlens, 64)
+    with pytest.raises(ValueError, match="out"):
+        A.prefill_varlen(x.q, x.k, x.v, x.cu_seqlens, 64, out=torch.empty_like(x.q[:5]))
+    kc = torch.zeros(4, 16, 8, 128, dtype=torch.bfloat16, device=DEV)
+    nk = torch.zeros(3, 8, 128, dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(ValueError, match="slot_mapping"):
+        A.cache_append(nk, nk, kc, kc.clone(), torch.zeros(2, dtype=torch.int64, device=DEV))
+    with pytest.raises(ValueError, match="new_k"):
+        A.cache_append(nk[:, :4].contiguous(), nk[:, :4].contiguous(), kc, kc.clone(),
+                       torch.zeros(3, dtype=torch.int64, device=DEV))
+
+
+def test_two_streams_in_flight_do_not_share_workspace():
+    """Prefill and decode launched concurrently on two streams (the header's reentrancy promise):
+    each stream gets its own workspace, so the self-resetting prefill counter and the decode
+    partials never collide — outputs equal the single-stream results exactly."""
+    xs = [W.make_prefill(dict(W.C3, batch_size=6, seq_len_min=100, seq_len_max=3000, seed=s), device=DEV)
+          for s in (1, 2)]
+    ds = [W.make_decode(dict(W.C2, batch_size=48, seq_len=2000, seed=s), device=DEV) for s in (3, 4)]
+    ref_p = [A.prefill_varlen(x.q, x.k, x.v, x.cu_seqlens, x.max_seqlen).clone() for x in xs]
+    ref_d = [A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens).clone() for d in ds]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for _ in range(5):
+        outs_p, outs_d = [None, None], [None, None]
+        for i, s in enumerate(streams):
+            with torch.cuda.stream(s):
+                outs_p[i] = A.prefill_varlen(xs[i].q, xs[i].k, xs[i].v, xs[i].cu_seqlens, xs[i].max_seqlen)
+                outs_d[i] = A.paged_decode(ds[i].q, ds[i].k_cache, ds[i].v_cache, ds[i].block_table, ds[i].seq_lens)
+        torch.cuda.synchronize()
+        for i in range(2):
+            assert torch.equal(outs_p[i], ref_p[i])
+            assert torch.equal(outs_d[i], ref_d[i])
+
+
+def test_decode_step_graph_matches_eager_api():
+    """DecodeStep (H2D -> cache_append -> paged_decode -> D2H in one CUDA graph) == the eager calls."""
+    lens = [700, 33, 4096, 1]
+    d = W.make_decode(dict(W.C2, batch_size=4, seq_len=4096), device=DEV, lens=lens, extra_blocks=2)
+    k2, v2 = d.k_cache.clone(), d.v_cache.clone()
+    step = A.DecodeStep(d.k_cache, d.v_cache, d.block_table, batch=4, num_q_heads=32)
+    g = torch.Generator().manual_seed(1)
+    bs = 16
+    bt = d.block_table.cpu()
+    for it in range(3):
+        q = torch.randn(4, 32, 128, generator=g).bfloat16()
+        nk, nv = (torch.randn(4, 8, 128, generator=g).bfloat16() for _ in range(2))
+        slots = torch.tensor([int(bt[b, (n - 1) // bs]) * bs + (n - 1) % bs for b, n in enumerate(lens)])
+        step.q_host.copy_(q)
+        step.new_k_host.copy_(nk)
+        step.new_v_host.copy_(nv)
+        step.slots_host.copy_(slots)
+        step.seq_lens_host.copy_(torch.tensor(lens, dtype=torch.int32))
+        out = step(sync=True).clone()
+        A.cache_append(nk.to(DEV), nv.to(DEV), k2, v2, slots.to(DEV))
+        ref = A.paged_decode(q.to(DEV), k2, v2, d.block_table, d.seq_lens)
+        assert torch.equal(d.k_cache, k2) and torch.equal(d.v_cache, v2)
+        assert torch.equal(out, ref.cpu())
+    o = oracle.decode(q, k2.cpu(), v2.cpu(), bt, torch.tensor(lens, dtype=torch.int32))
+    assert np.abs(out.float().numpy() - o).max() < 1e-2
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _bench_2rank(backend, extra_env=None):
+    env = dict(os.environ, PYTHONPATH=str(ROOT), **(extra_env or {}))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"), "--gpus", "2", "--steps", "4",
+           "--warmup", "3", "--no-cpu-baseline", "--dist-backend", backend]
+    r = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    return lines[0]
+
+
+def _check_2rank_line(line):
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
+    c4, c3 = line["extra"]["c4_strong"], line["extra"]["c3_heads_strong"]
+    assert c4["seqs_per_rank"] == 128 and c4["validation"]["pass"], c4
+    assert c3["kv_heads"] == [0, 4] and c3["validation"]["pass"], c3
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs (NCCL ranks)")
+def test_bench_two_ranks_nccl():
+    _check_2rank_line(_bench_2rank("nccl"))
+
+
+def test_bench_two_ranks_one_gpu_gloo():
+    """The N>1 host path (torchrun ranks, barriers, max-over-ranks timing, C4 batch shards and C3
+    kv-head shards, gather to rank 0, oracle validation) with both ranks on one GPU (gloo)."""
+    _check_2rank_line(_bench_2rank("gloo", {"B200_BENCH_ALLOW_SHARED_GPU": "1"}))

@@ -110,3 +110,31 @@ def test_fp8_decode_equals_bf16_decode_on_dequantised_cache():
     assert torch.equal(kb.float(), d.k_cache.float() * d.k_scale)
     b = oracle.decode(d.q, kb, vb, d.block_table, d.seq_lens)
     assert np.abs(a - b).max() < 1e-12
+
+
+def test_blas_prefill_equals_c_oracle():
+    """The chunked-BLAS fp64 restatement (used by the full-size GPU parity tests) == the C oracle."""
+    x = W.make_prefill(dict(W.C1, batch_size=3, seq_len=70, num_q_heads=8, num_kv_heads=2), device="cpu")
+    x.cu_seqlens[:] = torch.tensor([0, 1, 70, 210], dtype=torch.int32)
+    for causal in (True, False):
+        a = oracle.prefill(x.q, x.k, x.v, x.cu_seqlens, causal=causal)
+        b = oracle.prefill_blas(x.q, x.k, x.v, x.cu_seqlens, causal=causal, chunk=32)
+        assert np.abs(a - b).max() < 1e-12
+        c = oracle.prefill_blas(x.q, x.k, x.v, x.cu_seqlens, causal=causal, heads=[1, 6])
+        assert np.abs(a[:, [1, 6]] - c).max() < 1e-12
+
+
+def test_torch_cpu_sdpa_matches_oracle():
+    """oracle/torch_cpu.py (the PyTorch-native CPU baseline, fp32) agrees with the fp64 oracle."""
+    import torch_cpu
+
+    x = W.make_prefill(dict(W.C1, batch_size=2, seq_len=150, num_q_heads=8, num_kv_heads=2), device="cpu")
+    x.cu_seqlens[:] = torch.tensor([0, 40, 300], dtype=torch.int32)
+    ref = oracle.prefill(x.q, x.k, x.v, x.cu_seqlens)
+    assert np.abs(torch_cpu.prefill(x.q, x.k, x.v, x.cu_seqlens).double().numpy() - ref).max() < 1e-5
+    d = W.make_decode(dict(W.C2, batch_size=3, seq_len=300), device="cpu", lens=[300, 1, 33], extra_blocks=2)
+    ref = oracle.decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)
+    out = torch_cpu.decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)
+    assert np.abs(out.double().numpy() - ref).max() < 1e-5
+    out = torch_cpu.decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens, dtype=torch.bfloat16)
+    assert np.abs(out.double().numpy() - ref).max() < 2e-2  # bf16 output rounding
