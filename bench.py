@@ -448,8 +448,9 @@ def run_reference(args, world, rank):
 
 
 # ----------------------------------------------------------------------------- validation (rank 0)
-def validate_c4(shape, out_full, check_seqs):
-    """rank 0: rebuild the checked sequences from their seeds and compare with the fp64 oracle."""
+def validate_c4(shape, out_full, check_seqs, gen_device="cpu"):
+    """rank 0: rebuild the checked sequences from their seeds (on the device type that generated
+    the shards: CUDA and CPU generators differ) and compare with the fp64 oracle."""
     import torch
 
     import oracle
@@ -457,7 +458,7 @@ def validate_c4(shape, out_full, check_seqs):
 
     worst_abs, worst_rel = 0.0, 0.0
     for b in check_seqs:
-        q, k, v = W.decode_sequence(shape, b, device="cpu")
+        q, k, v = (t.cpu() for t in W.decode_sequence(shape, b, device=gen_device))
         n, Hkv, D = k.shape
         bs = int(shape.get("block_size", 16))
         nb = (n + bs - 1) // bs
@@ -472,7 +473,7 @@ def validate_c4(shape, out_full, check_seqs):
             "tolerance_max_abs": PARITY_TOL, "pass": worst_abs <= PARITY_TOL}
 
 
-def validate_c3_heads(shape, out_full_hTd, checks):
+def validate_c3_heads(shape, out_full_hTd, checks, gen_device="cpu"):
     """rank 0: out_full [Hq, T, D] gathered over head shards; checks = [(seq, kv_head)]."""
     import torch
 
@@ -486,7 +487,7 @@ def validate_c3_heads(shape, out_full_hTd, checks):
     G = int(shape["num_q_heads"]) // int(shape["num_kv_heads"])
     worst_abs, worst_rel = 0.0, 0.0
     for s, kvh in checks:
-        q, k, v = W.prefill_kv_head(shape, kvh, device="cpu")
+        q, k, v = (t.cpu() for t in W.prefill_kv_head(shape, kvh, device=gen_device))
         a, b = cu[s], cu[s + 1]
         ref = oracle.prefill_blas(q[a:b], k[a:b], v[a:b], torch.tensor([0, b - a], dtype=torch.int32))
         got = out_full_hTd[kvh * G:(kvh + 1) * G, a:b].transpose(0, 1)
@@ -528,7 +529,7 @@ def c4_strong(args, world, rank, dev, stream, steps, pk):
     torch.cuda.synchronize()
     full = parallel.gather_to_rank0(out, counts)  # NCCL gather: validation only, outside the timed region
     if rank == 0 and not args.no_validate:
-        res["validation"] = validate_c4(shape, full, (0, total // 2 + 1, total - 1))
+        res["validation"] = validate_c4(shape, full, (0, total // 2 + 1, total - 1), gen_device=dev)
     return res, plan, d
 
 
@@ -565,7 +566,7 @@ def c3_heads_strong(args, world, rank, dev, stream, steps, pk):
     counts = [len(parallel.kv_head_groups(Hkv, world, r)) * (Hq // Hkv) for r in range(world)]
     full = parallel.gather_to_rank0(out.transpose(0, 1).contiguous(), counts)  # [Hq, T, D] on rank 0
     if rank == 0 and not args.no_validate:
-        res["validation"] = validate_c3_heads(shape, full, [(0, 0), (8, Hkv - 1), (15, 0)])
+        res["validation"] = validate_c3_heads(shape, full, [(0, 0), (8, Hkv - 1), (15, 0)], gen_device=dev)
     del plan, x, g
     return res
 

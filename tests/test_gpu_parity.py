@@ -1,12 +1,18 @@
 """GPU parity: the sm_100a kernels (through the C ABI) vs the CPU oracle on identical inputs.
 
-Tolerance (bf16 in, fp32 accumulate, bf16 out), per case:
-  * max-abs error <= 2 x (max-abs error of torch SDPA run in bf16 on the same inputs) + 1e-4, and
-  * max-rel error  = max |out - ref| / max(|ref|, 1)  <= 1e-2.
-Errors are printed per case (pytest -s) so the report has the numbers.
-Full-size configs (C2, C3, C4-shard) are checked on seeded subsets against the oracle (heads and
-sequences are independent, so a slice is an exact sub-problem) and through size-independent
-properties: split-count invariance, physical-page permutation invariance (bit-exact).
+Tolerance (BASELINE.md §4; bf16 in, fp32 accumulate, bf16 out), per case:
+  * max-abs error <= 2 x (max-abs error of torch SDPA run in bf16 on the same inputs) + 1e-4;
+  * max-abs error <= 1e-2 beyond the bf16 output quantum: every element satisfies
+    |out - ref| <= 1e-2 + ulp_bf16(ref) / 2.  The plain max-abs <= 1e-2 is asserted on every
+    BASELINE configuration (C1, C2, C3, C4) and golden vector; only inputs that drive |O| past 2
+    (score-jump and small-sequence GQA cases, where bf16's own rounding is up to 1.6e-2 and SDPA in
+    bf16 misses 1e-2 by the same amount) use the quantum-aware form — BASELINE.md §4 amendment;
+  * max-rel error = max |out - ref| / max(|ref|, 1) <= 1e-2.
+Errors are printed per case (pytest -s) and tabulated at the end of the run (tests/conftest.py).
+Full-size configs are checked IN FULL against the oracle: C1, C2 (all 64 sequences), C3 (all 16
+sequences x 32 q heads, through the BLAS fp64 restatement), a 32-sequence C4 shard (the per-GPU
+load at 8 GPUs), and the whole 256-sequence C4 on one GPU on a seeded subset; plus properties:
+split-count invariance, physical-page permutation invariance (bit-exact).
 """
 import glob
 import json
@@ -70,16 +76,34 @@ def sdpa_decode_bf16(q, kc, vc, bt, sl):
     return out.numpy()
 
 
+PARITY_TOL = 1e-2
+RESULTS = []  # (name, max_abs, max_rel, sdpa_bf16_max_abs, max_abs_beyond_quantum, strict) -> conftest summary
+
+
+def bf16_half_ulp(x: np.ndarray) -> np.ndarray:
+    """half the spacing of bf16 numbers at |x| (8 significant bits)."""
+    e = np.floor(np.log2(np.maximum(np.abs(x), 2.0 ** -126)))
+    return 2.0 ** (e - 8)
+
+
 def check(name, out, ref, base):
+    """strict: plain max-abs <= 1e-2 (BASELINE configs, goldens).  Otherwise the 1e-2 bound applies
+    beyond bf16's own output rounding (see module docstring)."""
     out = out.float().cpu().numpy() if isinstance(out, torch.Tensor) else out
     err = np.abs(out - ref)
     base_err = np.abs(base - ref).max()
     rel = (err / np.maximum(np.abs(ref), 1.0)).max()
+    beyond = (err - bf16_half_ulp(ref)).max()
     print(f"[parity] {name}: max_abs={err.max():.3e} max_rel={rel:.3e} mean_abs={err.mean():.2e} "
-          f"sdpa_bf16_max_abs={base_err:.3e}")
+          f"sdpa_bf16_max_abs={base_err:.3e} beyond_bf16_quantum={beyond:.3e}")
+    RESULTS.append((name, float(err.max()), float(rel), float(base_err), float(beyond), strict))
     assert not np.isnan(out).any(), name
     assert err.max() <= 2 * base_err + 1e-4, (name, err.max(), base_err)
     assert rel <= 1e-2, (name, rel)
+    if strict:
+        assert err.max() <= PARITY_TOL, (name, err.max())
+    else:
+        assert beyond <= PARITY_TOL, (name, beyond)
 
 
 def run_prefill(lens, Hq=32, Hkv=8, causal=True, cfg=None, seed=1):
@@ -152,7 +176,7 @@ def test_golden(path):
         sl = torch.from_numpy(z["seq_lens"]).to(DEV)
         out = A.paged_decode(q, kc, vc, bt, sl)
         base = sdpa_decode_bf16(q, kc, vc, bt, sl)
-    check(Path(path).stem, out, z["out"].astype(np.float64), base)
+    check(Path(path).stem, out, z["out"].astype(np.float64), base, strict=True)
 
 
 # ------------------------------------------------------------------ prefill
@@ -228,26 +252,20 @@ def test_prefill_c1_full():
     ref = oracle.prefill(x.q, x.k, x.v, x.cu_seqlens)
     qd, kd, vd = x.q.to(DEV), x.k.to(DEV), x.v.to(DEV)
     out = A.prefill_varlen(qd, kd, vd, x.cu_seqlens.to(DEV), x.max_seqlen)
-    check("C1 full", out, ref, sdpa_prefill_bf16(qd, kd, vd, x.cu_seqlens, True))
+    check("C1 full", out, ref, sdpa_prefill_bf16(qd, kd, vd, x.cu_seqlens, True), strict=True)
 
 
 @pytest.mark.parametrize("cfg", [None, pcfg(256, 128, 2, nw=8)], ids=["dispatch", "bm256w8"])
-def test_prefill_c3_full_size_subset(cfg):
-    """Run all of C3 (16 seqs, 33430 tokens) on the GPU; check the shortest, a middle and the
-    longest sequence on kv heads {0, 7} (their 8 q heads) against the oracle."""
+def test_prefill_c3_full(cfg):
+    """All of C3 (16 seqs, 33430 tokens, 32 q heads) on the GPU vs the fp64 oracle on EVERY
+    sequence and head (oracle.prefill_blas: the BLAS restatement, pinned to the C oracle in
+    tests/test_oracle.py).  SDPA-bf16's error is computed on the same full problem."""
     x = W.make_prefill(W.C3, device="cpu")
-    out = A.prefill_varlen(x.q.to(DEV), x.k.to(DEV), x.v.to(DEV), x.cu_seqlens.to(DEV), x.max_seqlen,
-                           config=cfg).cpu()
-    cu = x.cu_seqlens.tolist()
-    for s in (0, 8, 15):
-        a, b = cu[s], cu[s + 1]
-        for kvh in (0, 7):
-            hs = slice(kvh * 4, kvh * 4 + 4)
-            qq, kk, vv = x.q[a:b, hs].contiguous(), x.k[a:b, kvh:kvh + 1].contiguous(), x.v[a:b, kvh:kvh + 1].contiguous()
-            cu1 = torch.tensor([0, b - a], dtype=torch.int32)
-            ref = oracle.prefill(qq, kk, vv, cu1)
-            base = sdpa_prefill_bf16(qq.to(DEV), kk.to(DEV), vv.to(DEV), cu1, True)
-            check(f"C3 seq{s} (L={b - a}) kvh{kvh}", out[a:b, hs], ref, base)
+    qd, kd, vd, cud = x.q.to(DEV), x.k.to(DEV), x.v.to(DEV), x.cu_seqlens.to(DEV)
+    out = A.prefill_varlen(qd, kd, vd, cud, x.max_seqlen, config=cfg).cpu()
+    ref = oracle.prefill_blas(x.q, x.k, x.v, x.cu_seqlens)
+    base = sdpa_prefill_bf16(qd, kd, vd, x.cu_seqlens, True)
+    check(f"C3 full (16 seqs x 32 heads) {'dispatch' if cfg is None else 'bm256w8'}", out, ref, base, strict=True)
 
 
 # ------------------------------------------------------------------ decode
@@ -356,29 +374,59 @@ def test_decode_nan_in_unused_page_slots(tile):
 
 
 def test_decode_c2_full_size():
-    """C2 in full on the GPU; 4 sequences vs the oracle; split-count invariance on all 64."""
+    """C2 in full on the GPU, ALL 64 sequences vs the oracle (flat K2'+K3' and the split K2+K3
+    paths); split-count invariance on all 64."""
     d = W.make_decode(W.C2, device="cpu")
     args = [t.to(DEV) for t in (d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)]
     outs = {s: A.paged_decode(*args, config=dcfg(s)).float() for s in (1, 2, 8, 0)}
     outs["flat"] = A.paged_decode(*args, config=FLAT).float()
     for s in (2, 8, 0, "flat"):
         assert (outs[s] - outs[1]).abs().max().item() < 2e-2
-    sub = [0, 21, 42, 63]
-    bt = d.block_table[sub]
-    ref = oracle.decode(d.q[sub], d.k_cache, d.v_cache, bt, d.seq_lens[sub])
-    base = sdpa_decode_bf16(args[0][sub], args[1], args[2], args[3][sub], args[4][sub])
-    check("C2 full (4 seqs checked) split", outs[0][sub], ref, base)
-    check("C2 full (4 seqs checked) flat", outs["flat"][sub], ref, base)
-
-
-def test_decode_c4_shard_subset():
-    """C4 geometry (64q/8kv, ctx 32k) on a 2-sequence shard vs the oracle."""
-    shape = dict(W.C4, batch_size=2)
-    d = W.make_decode(shape, device="cpu")
-    args = [t.to(DEV) for t in (d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)]
-    out = A.paged_decode(*args)
     ref = oracle.decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)
-    check("C4 shard (2 x 32k)", out, ref, sdpa_decode_bf16(*args))
+    base = sdpa_decode_bf16(*args)
+    check("C2 full (64 seqs) split", outs[0], ref, base, strict=True)
+    check("C2 full (64 seqs) flat", outs["flat"], ref, base, strict=True)
+
+
+def test_decode_c4_shard_full():
+    """The per-GPU load of C4 at 8 GPUs — 32 sequences x ctx 32768, 64q/8kv (4.3 GB of K+V; each
+    sequence spans ~5 of the flat partition's CTAs) — every sequence vs the oracle."""
+    shape = dict(W.C4, batch_size=32)
+    d = W.make_decode(shape, device=DEV)
+    out = A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)
+    cpu = [t.cpu() for t in (d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)]
+    ref = oracle.decode(*cpu)
+    sub = list(range(0, 32, 8))  # SDPA-bf16 reference error on a subset (it gathers per sequence)
+    base = sdpa_decode_bf16(d.q[sub], d.k_cache, d.v_cache, d.block_table[sub], d.seq_lens[sub])
+    err = np.abs(out.float().cpu().numpy() - ref)
+    base_err = np.abs(base - ref[sub]).max()
+    rel = (err / np.maximum(np.abs(ref), 1.0)).max()
+    print(f"[parity] C4 shard (32 x 32k) all seqs: max_abs={err.max():.3e} max_rel={rel:.3e} "
+          f"sdpa_bf16_max_abs(4 seqs)={base_err:.3e}")
+    RESULTS.append(("C4 shard (32 x 32k, 64q/8kv) all 32 seqs", float(err.max()), float(rel), float(base_err),
+                    float((err - bf16_half_ulp(ref)).max()), True))
+    assert err.max() <= PARITY_TOL and err.max() <= 2 * base_err + 1e-4 and rel <= 1e-2
+
+
+def test_decode_c4_full_one_gpu_seeded_subset():
+    """The whole C4 (256 sequences x 32k, 34.4 GB of K+V) on one B200 through the sharded builder
+    (every sequence's content is a function of its global index); 8 sequences spread over the batch
+    are rebuilt on the host from their seeds and checked against the oracle."""
+    shape = dict(W.C4)
+    d = W.make_decode_shard(shape, 0, 256, device=DEV)
+    out = A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens).cpu()
+    del d
+    torch.cuda.empty_cache()
+    worst = 0.0
+    for b in (0, 37, 100, 127, 128, 200, 254, 255):
+        q, k, v = (t.cpu() for t in W.decode_sequence(shape, b, device=DEV))  # same generator as the shard
+        nb = k.shape[0] // 16
+        ref = oracle.decode(q[None], k.view(nb, 16, 8, 128), v.view(nb, 16, 8, 128),
+                            torch.arange(nb, dtype=torch.int32)[None], torch.tensor([k.shape[0]], dtype=torch.int32))
+        worst = max(worst, float(np.abs(out[b:b + 1].float().numpy() - ref).max()))
+    print(f"[parity] C4 full (256 x 32k) 8 seeded seqs: max_abs={worst:.3e}")
+    RESULTS.append(("C4 full (256 x 32k) 8 seeded seqs", worst, worst, float("nan"), worst, True))
+    assert worst <= PARITY_TOL
 
 
 @pytest.mark.parametrize("tile", [16, 128])
