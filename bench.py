@@ -572,7 +572,7 @@ def c3_heads_strong(args, world, rank, dev, stream, steps, pk):
 
 
 # ----------------------------------------------------------------------------- e2e (public API, host buffers)
-def e2e_decode(d, dev, world, stream, n_steps):
+def e2e_decode(d, dev, world, stream, n_steps, chunks=0):
     """One serving step through the public API with HOST buffers, captured as ONE CUDA graph
     (attention.DecodeStep): H2D of q / new K,V / slots / seq_lens from a pinned buffer, cache_append,
     paged_decode, D2H of the output.  The block table stays resident (a serving loop updates one
@@ -590,13 +590,9 @@ def e2e_decode(d, dev, world, stream, n_steps):
     slots = torch.tensor([int(bt_host[b, (n - 1) // bs]) * bs + (n - 1) % bs for b, n in enumerate(d.lens)],
                          dtype=torch.int64)
     step = A.DecodeStep(d.k_cache, d.v_cache, d.block_table, batch=B, num_q_heads=Hq, max_seq_len=d.max_seq_len,
-                        k_scale=d.k_scale, v_scale=d.v_scale)
+                        k_scale=d.k_scale, v_scale=d.v_scale, chunks=chunks)
     # the host-side inputs of a step live in the step's pinned staging buffer
-    step.q_host.copy_(d.q.cpu())
-    step.new_k_host.copy_(new_k)
-    step.new_v_host.copy_(new_v)
-    step.slots_host.copy_(slots)
-    step.seq_lens_host.copy_(d.seq_lens.cpu())
+    step.set_inputs(d.q.cpu(), new_k, new_v, slots, d.seq_lens.cpu())
     for _ in range(3):
         step()
     torch.cuda.synchronize()
@@ -609,9 +605,10 @@ def e2e_decode(d, dev, world, stream, n_steps):
     out = step.out_host.clone()
     return {"value": world * d.kv_bytes / (e_ms / 1e3) / 1e9, "unit": "GB/s",
             "h2d_bytes_per_step": step.h2d_bytes, "d2h_bytes_per_step": step.d2h_bytes, "ms_per_step": e_ms,
+            "chunks": step.chunks,
             "path": "paper_2505_03780_b200.DecodeStep (public API: one CUDA graph of H2D copy from pinned host "
-                    "memory -> cache_append -> paged_decode -> D2H copy of the output); paged KV pool and block "
-                    "table resident in HBM"}, out
+                    "memory -> cache_append -> paged_decode -> D2H copy of the output, the batch in chunks whose "
+                    "copies overlap the other chunks' kernels); paged KV pool and block table resident in HBM"}, out
 
 
 # ----------------------------------------------------------------------------- the B200 arm
@@ -708,7 +705,8 @@ def run_b200(args, world, rank, local, gpu):
 
     # ------------------------------------------------------------------ e2e through the public API
     if d is not None:
-        e2e, _ = e2e_decode(d, dev, world, stream, max(10, args.steps // 5) if args.workload == "decode" else 5)
+        e2e, _ = e2e_decode(d, dev, world, stream, max(10, args.steps // 5) if args.workload == "decode" else 5,
+                            chunks=args.e2e_chunks)
         if scaling == "strong":
             e2e["value"] = 2 * 256 * 32768 * 8 * 128 * 2 / (e2e["ms_per_step"] / 1e3) / 1e9
     else:
@@ -827,6 +825,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-validate", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=0, help="DecodeStep chunks (0 = auto)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample size (seconds)")
     ap.add_argument("--cpu-step-seconds", type=float, default=0.2, help="reference arm: seconds per step")
     args = ap.parse_args()

@@ -433,41 +433,83 @@ class DecodeStep:
         H2D (pinned staging: q, the new token's K/V, slot_mapping, seq_lens)
         -> cache_append (new K/V into its page slot) -> paged_decode -> D2H (output, pinned)
 
-    The caller writes this step's inputs into ``q_host`` / ``new_k_host`` / ``new_v_host`` /
-    ``slots_host`` / ``seq_lens_host`` and calls the object; ``out_host`` holds the result once the
-    stream reaches the end of the step (``sync=True`` waits for it).  The paged KV pool and the
-    block table stay resident on the device: a serving loop appends one page index per sequence
-    every ``block_size`` steps, in place.  One graph replay = 1 memcpy + 2-3 kernels + 1 memcpy,
-    no per-call host work beyond the replay itself."""
+    The batch is cut into ``chunks`` contiguous groups of sequences whose transfers overlap the
+    other groups' kernels on separate copy streams: H2D(i+1) runs under decode(i) and D2H(i) under
+    decode(i+1), so only the first group's inputs and the last group's output sit on the critical
+    path.  The graph is: copy stream H2D_i -> event -> compute stream append_i, decode_i -> event ->
+    copy stream D2H_i, joined back at the end.
+
+    Inputs are written through ``set_inputs`` (or the per-chunk host views ``chunk_views(i)``);
+    ``out_host`` [B, Hq, D] holds the result once the stream reaches the end of the step
+    (``sync=True`` waits for it).  The paged KV pool and the block table stay resident on the
+    device: a serving loop appends one page index per sequence every ``block_size`` steps, in place."""
 
     def __init__(self, k_cache, v_cache, block_table, batch: int, num_q_heads: int, max_seq_len=None, config=None,
-                 softmax_scale=None, k_scale=None, v_scale=None):
+                 softmax_scale=None, k_scale=None, v_scale=None, chunks: int = 0):
         dev = k_cache.device
         _check_cache(k_cache, "k_cache")
         Hkv, D = k_cache.shape[2], k_cache.shape[3]
         B, Hq = int(batch), int(num_q_heads)
-        proto = (torch.empty(B, Hq, D, dtype=torch.bfloat16), torch.empty(B, Hkv, D, dtype=torch.bfloat16),
-                 torch.empty(B, Hkv, D, dtype=torch.bfloat16), torch.full((B,), -1, dtype=torch.int64),
-                 torch.zeros(B, dtype=torch.int32))
-        self.stage_h, views = pack_pinned(proto)
-        self.q_host, self.new_k_host, self.new_v_host, self.slots_host, self.seq_lens_host = (
-            unpack_view(self.stage_h, v) for v in views)
+        if chunks <= 0:
+            chunks = 2 if B >= 32 else 1
+        chunks = max(1, min(chunks, B))
+        bounds = [B * i // chunks for i in range(chunks + 1)]
+        self.bounds = bounds
+        self.chunks = chunks
+        # chunk-major pinned staging: chunk i = [q | new_k | new_v | slots | seq_lens] of its rows
+        protos, self._views = [], []
+        for i in range(chunks):
+            n = bounds[i + 1] - bounds[i]
+            protos += [torch.empty(n, Hq, D, dtype=torch.bfloat16), torch.empty(n, Hkv, D, dtype=torch.bfloat16),
+                       torch.empty(n, Hkv, D, dtype=torch.bfloat16), torch.full((n,), -1, dtype=torch.int64),
+                       torch.zeros(n, dtype=torch.int32)]
+        self.stage_h, views = pack_pinned(protos)
         self.stage_d = torch.empty_like(self.stage_h, device=dev)
-        q_d, nk_d, nv_d, slots_d, sl_d = (unpack_view(self.stage_d, v) for v in views)
         self.out_host = torch.empty(B, Hq, D, dtype=torch.bfloat16).pin_memory()
-        self.h2d_bytes = self.stage_h.numel()
+        self.out_d = torch.empty(B, Hq, D, dtype=torch.bfloat16, device=dev)
+        self.h2d_bytes = sum(math.prod(v[1]) * torch.empty(0, dtype=v[2]).element_size() for v in views)
         self.d2h_bytes = self.out_host.numel() * 2
-        self.plan = DecodePlan(q_d, k_cache, v_cache, block_table, sl_d, max_seq_len=max_seq_len, config=config,
-                               softmax_scale=softmax_scale, k_scale=k_scale, v_scale=v_scale)
         self.device = dev
+        self.plans, ranges = [], []
+        for i in range(chunks):
+            hv = [unpack_view(self.stage_h, v) for v in views[5 * i:5 * i + 5]]
+            dv = [unpack_view(self.stage_d, v) for v in views[5 * i:5 * i + 5]]
+            self._views.append(hv)
+            lo = views[5 * i][0]
+            last = views[5 * i + 4]
+            hi = last[0] + math.prod(last[1]) * 4
+            ranges.append((lo, hi))
+            b0, b1 = bounds[i], bounds[i + 1]
+            self.plans.append((DecodePlan(dv[0], k_cache, v_cache, block_table[b0:b1], dv[4], out=self.out_d[b0:b1],
+                                          max_seq_len=max_seq_len, config=config, softmax_scale=softmax_scale,
+                                          k_scale=k_scale, v_scale=v_scale), dv))
+        self.config = self.plans[0][0].config
 
         def body():
-            self.stage_d.copy_(self.stage_h, non_blocking=True)
-            cache_append(nk_d, nv_d, k_cache, v_cache, slots_d, k_scale=k_scale, v_scale=v_scale)
-            self.plan.run()
-            self.out_host.copy_(self.plan.out, non_blocking=True)
+            main = torch.cuda.current_stream(dev)
+            ev_in = [torch.cuda.Event() for _ in range(chunks)]
+            ev_dec = [torch.cuda.Event() for _ in range(chunks)]
+            self._cin.wait_stream(main)
+            self._cout.wait_stream(main)
+            with torch.cuda.stream(self._cin):
+                for i, (lo, hi) in enumerate(ranges):
+                    self.stage_d[lo:hi].copy_(self.stage_h[lo:hi], non_blocking=True)
+                    ev_in[i].record()
+            for i, (plan, dv) in enumerate(self.plans):
+                main.wait_event(ev_in[i])
+                cache_append(dv[1], dv[2], k_cache, v_cache, dv[3], k_scale=k_scale, v_scale=v_scale)
+                plan.run()
+                ev_dec[i].record(main)
+            with torch.cuda.stream(self._cout):
+                for i in range(chunks):
+                    self._cout.wait_event(ev_dec[i])
+                    b0, b1 = bounds[i], bounds[i + 1]
+                    self.out_host[b0:b1].copy_(self.out_d[b0:b1], non_blocking=True)
+            main.wait_stream(self._cin)
+            main.wait_stream(self._cout)
 
         with _on(dev):
+            self._cin, self._cout = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
             s = torch.cuda.Stream(dev)
             s.wait_stream(torch.cuda.current_stream(dev))
             with torch.cuda.stream(s):
@@ -478,6 +520,18 @@ class DecodeStep:
             with torch.cuda.graph(self.graph):
                 body()
         self.done = torch.cuda.Event()
+
+    def chunk_views(self, i: int):
+        """host views (q, new_k, new_v, slot_mapping, seq_lens) of chunk i's rows in the staging buffer."""
+        return self._views[i]
+
+    def set_inputs(self, q=None, new_k=None, new_v=None, slot_mapping=None, seq_lens=None):
+        """Scatter full-batch host tensors into the chunk-major pinned staging buffer."""
+        for i in range(self.chunks):
+            b0, b1 = self.bounds[i], self.bounds[i + 1]
+            for dst, src in zip(self._views[i], (q, new_k, new_v, slot_mapping, seq_lens)):
+                if src is not None:
+                    dst.copy_(src[b0:b1])
 
     def __call__(self, sync: bool = False) -> torch.Tensor:
         with _on(self.device):
