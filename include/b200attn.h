@@ -93,7 +93,9 @@ typedef struct {
   const int32_t* block_table; /* [batch, max_blocks_per_seq]                         */
   const int32_t* seq_lens;    /* [batch] cached tokens incl. the current one         */
   void* o;                    /* [batch, num_q_heads, head_dim] bf16                 */
-  void* workspace;            /* split partials; b200attn_decode_workspace_size bytes */
+  void* workspace;            /* split partials (+ per-sequence arrival counters of the flat kernel);
+                                 b200attn_decode_workspace_size bytes, ZERO-FILLED once at allocation
+                                 (the counters reset themselves; one workspace per stream in flight) */
   size_t workspace_bytes;
   int32_t batch;
   int32_t num_q_heads;
@@ -124,7 +126,9 @@ int b200attn_decode_supported(const b200attn_decode_params* p, const b200attn_de
 size_t b200attn_prefill_workspace_size(const b200attn_prefill_params* p);
 int b200attn_prefill(const b200attn_prefill_params* p, const b200attn_prefill_variant* v, void* stream);
 
-/* K2 (+K3): paged split-KV decode; the combine runs iff the resolved num_splits > 1. */
+/* K2 (+K3): paged split-KV decode; the combine runs iff the resolved num_splits > 1.  tile_n 16 (K2'):
+ * split sequences are merged inside K2' by the CTA finishing their last piece when sequences span few
+ * CTAs (batch >= ~num_SMs / 8), else by the K3' combine launch. */
 size_t b200attn_decode_workspace_size(const b200attn_decode_params* p, const b200attn_decode_variant* v);
 int b200attn_decode_num_splits(const b200attn_decode_params* p, const b200attn_decode_variant* v);
 int b200attn_decode(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream);

@@ -361,7 +361,8 @@ class DecodePlan:
         self.p = _decode_params(q, k_cache, v_cache, block_table, seq_lens, self.out, self.max_seq_len, softmax_scale,
                                 k_scale=k_scale, v_scale=v_scale)
         nbytes = self.lib.b200attn_decode_workspace_size(self.p, self.var)
-        self.ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=q.device) if nbytes else None
+        # zeroed: the flat kernel's per-sequence arrival counters must start at 0 (they self-reset)
+        self.ws = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=q.device) if nbytes else None
         if self.ws is not None:
             self.p.workspace, self.p.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
         self.num_splits = int(self.lib.b200attn_decode_num_splits(self.p, self.var))

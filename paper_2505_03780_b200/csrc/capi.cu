@@ -364,7 +364,21 @@ constexpr int kFlatMinTiles = 2;
 
 size_t flat_workspace_bytes(const b200attn_decode_params* p) {
   const size_t slots = (size_t)num_sms() + p->batch;
-  return slots * p->num_q_heads * (128 + 2) * sizeof(float) + ((size_t)p->batch + 1) * sizeof(int32_t);
+  // partials, cu_tiles[B + 1], per-sequence arrival counters[B] (zero before first use; self-resetting)
+  return slots * p->num_q_heads * (128 + 2) * sizeof(float) + (2 * (size_t)p->batch + 1) * sizeof(int32_t);
+}
+
+// Merge split sequences inside K2' (last-arriving piece, no K3' launch) when sequences span few
+// CTAs: with ~ctas / B + 1 pieces each, the merging CTA reads a handful of partials at its tail.
+// B200ATTN_FLAT_MERGE=0/1 forces either path (A/B).
+bool flat_fused_merge(int batch, int ctas) {
+  static int force = -2;
+  if (force == -2) {
+    const char* e = getenv("B200ATTN_FLAT_MERGE");
+    force = (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : -1;
+  }
+  if (force >= 0) return force == 1;
+  return ctas <= 8 * batch;
 }
 
 using FlatLauncher = int (*)(const b200attn_decode_params*, bool combine, cudaStream_t);
@@ -404,6 +418,8 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
   a.part_o = reinterpret_cast<float*>(p->workspace);
   a.part_ml = a.part_o + slots * p->num_q_heads * 128;
   a.cu_tiles_out = reinterpret_cast<int32_t*>(a.part_ml + slots * p->num_q_heads * 2);
+  const bool fused = flat_fused_merge(p->batch, ctas);
+  a.seq_cnt = fused ? a.cu_tiles_out + p->batch + 1 : nullptr;
   a.batch = p->batch;
   a.block_size = p->block_size;
   a.max_blocks = p->max_blocks_per_seq;
@@ -417,7 +433,7 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
   kern<<<ctas, C::NTHREADS, C::SMEM_BYTES, stream>>>(mq, mk, mv, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "decode_flat launch");
-  if (combine) {
+  if (combine && !fused) {
     b200::flat_combine_kernel<C::NQ><<<dim3(p->batch, C::NQ), 128, 0, stream>>>(
         a.part_o, a.part_ml, a.cu_tiles_out, p->batch, ctas, reinterpret_cast<__nv_bfloat16*>(p->o));
     e = cudaGetLastError();

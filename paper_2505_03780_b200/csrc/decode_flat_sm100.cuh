@@ -37,6 +37,9 @@ struct FlatDecodeArgs {
   float* part_o;               // [(ctas + B), Hq, 128]
   float* part_ml;              // [(ctas + B), Hq, 2]  (max in log2 units, sum)
   int32_t* cu_tiles_out;       // [B + 1] (written by CTA 0 for the combine)
+  int32_t* seq_cnt;            // [B] arrival counters (zeroed workspace, self-resetting), or null:
+                               // non-null = the last CTA to finish a piece of a split sequence merges
+                               // it in place (no K3' launch)
   int32_t batch;
   int32_t block_size;
   int32_t max_blocks;
@@ -90,6 +93,91 @@ __device__ __forceinline__ void e4m3_split2(float x0, float x1, uint16_t& hi, ui
   asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h16) : "h"(hi));
   const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h16));
   asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"((x1 - hf.y) * 16.f), "f"((x0 - hf.x) * 16.f));
+}
+
+__device__ __forceinline__ bool flat_owns(int c, int ctas, int ntiles) {
+  return static_cast<long long>(c) * ntiles / ctas != (static_cast<long long>(c) + 1) * ntiles / ctas;
+}
+
+// Fused K3' (the 128 softmax/epilogue threads of a CTA that just wrote a partial piece of sequence
+// b): arrive on b's counter; the CTA whose arrival completes b merges every piece in place — its
+// own from registers (r, ml_s), the others' from L2 — and writes b's output.  In the flat partition
+// a sequence split between CTAs c and c+1 is finished last by c (its head piece ends c's range,
+// its tail piece starts c+1's), so merges land in the kernel's tail, one per CTA at most.
+// Loads are batched (QC q heads x 2 pieces, three loads each, all issued before any use): a
+// dependent load chain per piece is what made an earlier in-kernel merge L2-latency-bound.
+// Protocol: all threads fence their partial stores, barrier, one thread's atomicAdd; the merging
+// threads fence again and read other CTAs' partials with ld.global.cg (L2, never a stale L1 line).
+template <int NQ, int NP>
+__device__ __forceinline__ void flat_merge_if_last(const FlatDecodeArgs& args, const uint32_t (&r)[NQ],
+                                                   const float* ml_s, volatile int* flags, const int32_t* cu,
+                                                   int b, int ntiles, int row) {
+  constexpr int D = 128;
+  const int ctas = static_cast<int>(gridDim.x);
+  __threadfence();
+  named_bar_sync(1, 128);
+  if (row == 0) {
+    const int c0 = flat_cta_of(cu[b], ctas, ntiles), c1 = flat_cta_of(cu[b + 1] - 1, ctas, ntiles);
+    int pieces = 0;
+    for (int c = c0; c <= c1; ++c) pieces += flat_owns(c, ctas, ntiles);
+    const int last = atomicAdd(args.seq_cnt + b, 1) == pieces - 1;
+    if (last) args.seq_cnt[b] = 0;  // every arrival of this launch is in: reset for the next one
+    flags[8] = last;
+    flags[9] = c0;
+    flags[10] = c1;
+  }
+  named_bar_sync(1, 128);
+  if (!flags[8]) return;
+  __threadfence();
+  const int c0 = flags[9], c1 = flags[10], self = static_cast<int>(blockIdx.x);
+  constexpr int QC = NQ < 16 ? NQ : 16;
+#pragma unroll
+  for (int q0 = 0; q0 < NQ; q0 += QC) {
+    float M[QC], L[QC], acc[QC];
+#pragma unroll
+    for (int j = 0; j < QC; ++j) {
+      M[j] = ml_s[q0 + j];
+      L[j] = ml_s[NP + q0 + j];
+      acc[j] = __uint_as_float(r[q0 + j]) * args.out_scale;
+    }
+    auto fold = [&](float mp, float lp, float op, int j) {
+      const float mn = fmaxf(M[j], mp);
+      if (mn == -INFINITY) return;
+      const float wa = fast_exp2(M[j] - mn), wb = fast_exp2(mp - mn);
+      L[j] = fmaf(L[j], wa, lp * wb);
+      acc[j] = fmaf(acc[j], wa, op * wb);
+      M[j] = mn;
+    };
+    int c = c0;
+    while (c <= c1) {
+      // next two pieces owned by other CTAs
+      int ca = -1, cb = -1;
+      for (; c <= c1 && ca < 0; ++c)
+        if (c != self && flat_owns(c, ctas, ntiles)) ca = c;
+      for (; c <= c1 && cb < 0; ++c)
+        if (c != self && flat_owns(c, ctas, ntiles)) cb = c;
+      if (ca < 0) break;
+      const size_t sa = static_cast<size_t>(ca) + b, sb = static_cast<size_t>(cb < 0 ? ca : cb) + b;
+      float ma[QC], la[QC], oa[QC], mb[QC], lb[QC], ob[QC];
+#pragma unroll
+      for (int j = 0; j < QC; ++j) {
+        ma[j] = __ldcg(args.part_ml + (sa * NQ + q0 + j) * 2);
+        la[j] = __ldcg(args.part_ml + (sa * NQ + q0 + j) * 2 + 1);
+        oa[j] = __ldcg(args.part_o + (sa * NQ + q0 + j) * D + row);
+        mb[j] = __ldcg(args.part_ml + (sb * NQ + q0 + j) * 2);
+        lb[j] = __ldcg(args.part_ml + (sb * NQ + q0 + j) * 2 + 1);
+        ob[j] = __ldcg(args.part_o + (sb * NQ + q0 + j) * D + row);
+      }
+#pragma unroll
+      for (int j = 0; j < QC; ++j) {
+        fold(ma[j], la[j], oa[j], j);
+        if (cb >= 0) fold(mb[j], lb[j], ob[j], j);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < QC; ++j)
+      args.o[(static_cast<size_t>(b) * NQ + q0 + j) * D + row] = __float2bfloat16_rn(L[j] > 0.f ? acc[j] / L[j] : 0.f);
+  }
 }
 
 template <int G, int NSTAGE, bool FP8 = false>
@@ -164,6 +252,12 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
   const int T1 = static_cast<int>((static_cast<long long>(blockIdx.x) + 1) * ntiles / gridDim.x);
   if (blockIdx.x == 0)
     for (int b = threadIdx.x; b <= B; b += C::NTHREADS) args.cu_tiles_out[b] = cu[b];
+  if (args.seq_cnt != nullptr) {  // fused merge (no K3'): empty sequences get their zero output here
+    for (int b = blockIdx.x; b < B; b += gridDim.x)
+      if (cu[b + 1] == cu[b])
+        for (int i = threadIdx.x; i < NQ * D / 8; i += C::NTHREADS)
+          reinterpret_cast<uint4*>(args.o + static_cast<size_t>(b) * NQ * D)[i] = make_uint4(0, 0, 0, 0);
+  }
   if (T0 >= T1) return;  // more CTAs than tiles (uniform per CTA)
   // first sequence with tiles beyond T0
   int b_first;
@@ -527,6 +621,7 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
           args.part_ml[(slot * NQ + row) * 2 + 0] = ml_s[row];
           args.part_ml[(slot * NQ + row) * 2 + 1] = ml_s[NP + row];
         }
+        if (args.seq_cnt != nullptr) flat_merge_if_last<NQ, NP>(args, r, ml_s, flags, cu, b, ntiles, row);
       }
       named_bar_sync(1, 128);  // ml_s reads done before the next segment's epilogue rewrites it
     }
