@@ -367,6 +367,8 @@ class DecodePlan:
             self.p.workspace, self.p.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
         self.num_splits = int(self.lib.b200attn_decode_num_splits(self.p, self.var))
         self.device = q.device
+        # the params struct holds raw pointers: keep the tensors alive as long as the plan
+        self._tensors = (q, k_cache, v_cache, block_table, seq_lens, self.out)
 
     def kernels_per_run(self) -> int:
         return 2 if (self.num_splits > 1 or int(self.config["TILE_N"]) == 16) else 1
@@ -398,6 +400,7 @@ class PrefillPlan:
                               device=q.device)
         self.p.workspace, self.p.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
         self.device = q.device
+        self._tensors = (q, k, v, cu_seqlens, self.out)  # raw pointers in self.p: keep them alive
 
     def run(self, stream=None):
         with _on(self.device):

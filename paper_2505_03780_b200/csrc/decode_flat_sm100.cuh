@@ -133,12 +133,14 @@ __device__ __forceinline__ void flat_merge_if_last(const FlatDecodeArgs& args, c
   constexpr int QC = NQ < 16 ? NQ : 16;
 #pragma unroll
   for (int q0 = 0; q0 < NQ; q0 += QC) {
+    // pieces are folded in CTA order whoever merges (this CTA's own piece from registers at its
+    // position), so the fp32 result is bit-identical from launch to launch
     float M[QC], L[QC], acc[QC];
 #pragma unroll
     for (int j = 0; j < QC; ++j) {
-      M[j] = ml_s[q0 + j];
-      L[j] = ml_s[NP + q0 + j];
-      acc[j] = __uint_as_float(r[q0 + j]) * args.out_scale;
+      M[j] = -INFINITY;
+      L[j] = 0.f;
+      acc[j] = 0.f;
     }
     auto fold = [&](float mp, float lp, float op, int j) {
       const float mn = fmaxf(M[j], mp);
@@ -148,16 +150,25 @@ __device__ __forceinline__ void flat_merge_if_last(const FlatDecodeArgs& args, c
       acc[j] = fmaf(acc[j], wa, op * wb);
       M[j] = mn;
     };
+    auto fold_self = [&]() {
+#pragma unroll
+      for (int j = 0; j < QC; ++j) fold(ml_s[q0 + j], ml_s[NP + q0 + j], __uint_as_float(r[q0 + j]) * args.out_scale, j);
+    };
     int c = c0;
     while (c <= c1) {
-      // next two pieces owned by other CTAs
+      // the next two owned pieces in CTA order; this CTA's own piece is folded in between
       int ca = -1, cb = -1;
       for (; c <= c1 && ca < 0; ++c)
-        if (c != self && flat_owns(c, ctas, ntiles)) ca = c;
+        if (flat_owns(c, ctas, ntiles)) ca = c;
+      if (ca == self) {
+        fold_self();
+        continue;
+      }
       for (; c <= c1 && cb < 0; ++c)
-        if (c != self && flat_owns(c, ctas, ntiles)) cb = c;
+        if (flat_owns(c, ctas, ntiles)) cb = c;
       if (ca < 0) break;
-      const size_t sa = static_cast<size_t>(ca) + b, sb = static_cast<size_t>(cb < 0 ? ca : cb) + b;
+      const bool b_self = (cb == self);
+      const size_t sa = static_cast<size_t>(ca) + b, sb = static_cast<size_t>(cb < 0 || b_self ? ca : cb) + b;
       float ma[QC], la[QC], oa[QC], mb[QC], lb[QC], ob[QC];
 #pragma unroll
       for (int j = 0; j < QC; ++j) {
@@ -169,9 +180,12 @@ __device__ __forceinline__ void flat_merge_if_last(const FlatDecodeArgs& args, c
         ob[j] = __ldcg(args.part_o + (sb * NQ + q0 + j) * D + row);
       }
 #pragma unroll
-      for (int j = 0; j < QC; ++j) {
-        fold(ma[j], la[j], oa[j], j);
-        if (cb >= 0) fold(mb[j], lb[j], ob[j], j);
+      for (int j = 0; j < QC; ++j) fold(ma[j], la[j], oa[j], j);
+      if (b_self) {
+        fold_self();
+      } else if (cb >= 0) {
+#pragma unroll
+        for (int j = 0; j < QC; ++j) fold(mb[j], lb[j], ob[j], j);
       }
     }
 #pragma unroll

@@ -140,3 +140,25 @@ def test_bench_two_ranks_one_gpu_gloo():
     """The N>1 host path (torchrun ranks, barriers, max-over-ranks timing, C4 batch shards and C3
     kv-head shards, gather to rank 0, oracle validation) with both ranks on one GPU (gloo)."""
     _check_2rank_line(_bench_2rank("gloo", {"B200_BENCH_ALLOW_SHARED_GPU": "1"}))
+
+
+def test_plans_keep_their_tensors_alive():
+    """Plans hold raw pointers in their params struct; they must own references to the tensors
+    (a plan built from temporaries used to read freed memory)."""
+    import gc
+
+    def make():
+        d = W.make_decode(dict(W.C2, batch_size=64, seq_len=1000), device=DEV)
+        ref = A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens).clone()
+        x = W.make_prefill(dict(W.C1, seq_len=300), device=DEV)
+        pref = A.prefill_varlen(x.q, x.k, x.v, x.cu_seqlens, 300).clone()
+        return (A.DecodePlan(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens), ref,
+                A.PrefillPlan(x.q, x.k, x.v, x.cu_seqlens, 300), pref)
+
+    dp, ref, pp, pref = make()
+    gc.collect()
+    torch.cuda.empty_cache()
+    junk = torch.full((1 << 28,), 7, dtype=torch.uint8, device=DEV)  # reuse any freed blocks
+    assert torch.equal(dp.run(), ref)
+    assert torch.equal(pp.run(), pref)
+    del junk
