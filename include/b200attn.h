@@ -132,8 +132,9 @@ int b200attn_prefill(const b200attn_prefill_params* p, const b200attn_prefill_va
 size_t b200attn_decode_workspace_size(const b200attn_decode_params* p, const b200attn_decode_variant* v);
 int b200attn_decode_num_splits(const b200attn_decode_params* p, const b200attn_decode_variant* v);
 int b200attn_decode(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream);
-/* K2 alone: with num_splits > 1 it leaves the unnormalised partials in the workspace
- * (layout: part_o [batch*Hq, splits, 128] fp32 then part_ml [batch*Hq, splits, 2]) for b200attn_combine;
+/* K2 alone: with num_splits > 1 it leaves the unnormalised partials in the workspace (layout: a
+ * 4096-byte counter header, then part_o [batch*Hq, splits, 128] fp32, then part_ml [batch*Hq, splits, 2])
+ * for b200attn_combine;
  * with one split it writes O directly. */
 int b200attn_decode_partial(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream);
 

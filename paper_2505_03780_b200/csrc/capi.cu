@@ -37,6 +37,10 @@ struct NvtxRange {
 
 constexpr int kMaxSmem = 232448;  // 227 KB opt-in per CTA on sm_100a
 constexpr int kNumSMs = 148;
+// Every decode workspace starts with kFlatCounters int32 arrival counters (K2' in-kernel merge) at a
+// FIXED offset, so launches of different shapes / kernels sharing one workspace never read each
+// other's partials as counters (zero before first use; every launch leaves them zero).
+constexpr size_t kFlatCounters = 1024;  // == FlatCfg::MAXB
 
 thread_local char g_err[512] = "";
 
@@ -312,7 +316,9 @@ int launch_decode(const b200attn_decode_params* p, int splits, int tps, bool com
   a.seq_lens = p->seq_lens;
   a.o = reinterpret_cast<__nv_bfloat16*>(p->o);
   const size_t rows = (size_t)p->batch * p->num_q_heads;
-  a.part_o = reinterpret_cast<float*>(p->workspace);
+  // partials after the counter header every decode workspace starts with (see flat_workspace_bytes)
+  a.part_o = p->workspace ? reinterpret_cast<float*>(reinterpret_cast<int32_t*>(p->workspace) + kFlatCounters)
+                          : nullptr;
   a.part_ml = a.part_o ? a.part_o + rows * splits * D : nullptr;
   a.num_q_heads = p->num_q_heads;
   a.group = G;
@@ -362,10 +368,13 @@ int num_sms() {  // per device (cached; a process may drive several GPUs)
 
 constexpr int kFlatMinTiles = 2;
 
+// Flat workspace: per-sequence arrival counters at a FIXED offset (see kFlatCounters), then
+// partials, then cu_tiles.
+
 size_t flat_workspace_bytes(const b200attn_decode_params* p) {
   const size_t slots = (size_t)num_sms() + p->batch;
-  // partials, cu_tiles[B + 1], per-sequence arrival counters[B] (zero before first use; self-resetting)
-  return slots * p->num_q_heads * (128 + 2) * sizeof(float) + (2 * (size_t)p->batch + 1) * sizeof(int32_t);
+  return kFlatCounters * sizeof(int32_t) + slots * p->num_q_heads * (128 + 2) * sizeof(float) +
+         ((size_t)p->batch + 1) * sizeof(int32_t);
 }
 
 // Merge split sequences inside K2' (last-arriving piece, no K3' launch) when sequences span few
@@ -415,11 +424,12 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
   a.block_table = p->block_table;
   a.seq_lens = p->seq_lens;
   a.o = reinterpret_cast<__nv_bfloat16*>(p->o);
-  a.part_o = reinterpret_cast<float*>(p->workspace);
+  int32_t* counters = reinterpret_cast<int32_t*>(p->workspace);
+  a.part_o = reinterpret_cast<float*>(counters + kFlatCounters);
   a.part_ml = a.part_o + slots * p->num_q_heads * 128;
   a.cu_tiles_out = reinterpret_cast<int32_t*>(a.part_ml + slots * p->num_q_heads * 2);
   const bool fused = flat_fused_merge(p->batch, ctas);
-  a.seq_cnt = fused ? a.cu_tiles_out + p->batch + 1 : nullptr;
+  a.seq_cnt = fused ? counters : nullptr;
   a.batch = p->batch;
   a.block_size = p->block_size;
   a.max_blocks = p->max_blocks_per_seq;
@@ -657,7 +667,7 @@ size_t b200attn_decode_workspace_size(const b200attn_decode_params* p, const b20
   resolve_splits(p, v, c.split->smem, &s, &t);
   if (s <= 1) return 0;
   const size_t rows = (size_t)p->batch * p->num_q_heads;
-  return rows * s * (128 + 2) * sizeof(float);
+  return kFlatCounters * sizeof(int32_t) + rows * s * (128 + 2) * sizeof(float);
 }
 
 static int decode_impl(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream,
@@ -678,7 +688,8 @@ static int decode_impl(const b200attn_decode_params* p, const b200attn_decode_va
   int s, t;
   resolve_splits(p, v, c.split->smem, &s, &t);
   if (s > 1) {
-    const size_t need = (size_t)p->batch * p->num_q_heads * s * (128 + 2) * sizeof(float);
+    const size_t need =
+        kFlatCounters * sizeof(int32_t) + (size_t)p->batch * p->num_q_heads * s * (128 + 2) * sizeof(float);
     if (!p->workspace || p->workspace_bytes < need)
       return fail(B200ATTN_BAD_ARGS, "workspace %zu B < %zu B needed for %d splits", p->workspace_bytes, need, s);
   }

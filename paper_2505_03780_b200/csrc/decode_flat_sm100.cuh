@@ -106,17 +106,19 @@ __device__ __forceinline__ bool flat_owns(int c, int ctas, int ntiles) {
 // its tail piece starts c+1's), so merges land in the kernel's tail, one per CTA at most.
 // Loads are batched (QC q heads x 2 pieces, three loads each, all issued before any use): a
 // dependent load chain per piece is what made an earlier in-kernel merge L2-latency-bound.
-// Protocol: all threads fence their partial stores, barrier, one thread's atomicAdd; the merging
-// threads fence again and read other CTAs' partials with ld.global.cg (L2, never a stale L1 line).
+// Protocol: barrier (the partial stores of all 128 threads happen-before it), then one thread's
+// gpu-scope fence + atomicAdd (the fence is cumulative, so only one warp waits for the stores to
+// drain); the merging threads fence again and read other CTAs' partials with ld.global.cg (L2,
+// never a stale L1 line).
 template <int NQ, int NP>
 __device__ __forceinline__ void flat_merge_if_last(const FlatDecodeArgs& args, const uint32_t (&r)[NQ],
                                                    const float* ml_s, volatile int* flags, const int32_t* cu,
                                                    int b, int ntiles, int row) {
   constexpr int D = 128;
   const int ctas = static_cast<int>(gridDim.x);
-  __threadfence();
-  named_bar_sync(1, 128);
+  named_bar_sync(1, 128);  // every thread's partial stores happen-before thread 0's fence (cumulative)
   if (row == 0) {
+    __threadfence();
     const int c0 = flat_cta_of(cu[b], ctas, ntiles), c1 = flat_cta_of(cu[b + 1] - 1, ctas, ntiles);
     int pieces = 0;
     for (int c = c0; c <= c1; ++c) pieces += flat_owns(c, ctas, ntiles);
