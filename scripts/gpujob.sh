@@ -11,6 +11,7 @@
 #   ncupf      ncu --set full of K1 on C3                       ncudec    ncu --set full of K2' on C2
 #   sanitize   compute-sanitizer memcheck/racecheck/synccheck on small cases of every kernel
 #   sota       scripts/sota.py (same-box library comparators)   single    single-launch vs amortised
+#   sotagrid   scripts/sota.py --grid (C5 grid, relative_cdf vs the best library per shape)
 #   perf       scripts/perf.py time over the BASELINE shapes
 set -u
 TAG=$1; shift
@@ -21,7 +22,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,temperature.gpu -
 for r in "$@"; do
   echo "== $r" >&2
   case $r in
-    tests) timeout 1500 python -m pytest tests -m gpu -x -q -rs > ${O}_tests.log 2>&1; tail -40 ${O}_tests.log ;;
+    tests) timeout 1500 python -m pytest tests -m gpu -q -rs > ${O}_tests.log 2>&1; tail -40 ${O}_tests.log ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > ${O}_smoke.log 2>&1; tail -3 ${O}_smoke.log ;;
     bench) timeout 900 python bench.py --steps 20 --warmup 5 > ${O}_bench.json 2> ${O}_bench.err; cat ${O}_bench.json; tail -5 ${O}_bench.err ;;
     benchref) timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > ${O}_benchref.json 2>&1; cat ${O}_benchref.json ;;
@@ -41,6 +42,7 @@ for r in "$@"; do
              -o ${O}_dec python scripts/perf.py prof --op decode > ${O}_ncudec.log 2>&1; tail -3 ${O}_ncudec.log ;;
     sanitize) timeout 2400 bash scripts/sanitize.sh ${O}_sanitize ;;
     sota) timeout 2400 python scripts/sota.py --out ${O}_sota.json > ${O}_sota.log 2>&1; tail -30 ${O}_sota.log ;;
+    sotagrid) timeout 2400 python scripts/sota.py --grid --out ${O}_sotagrid.json > ${O}_sotagrid.log 2>&1; tail -3 ${O}_sotagrid.log ;;
     single) timeout 600 python scripts/perf.py single --shapes C3,C1 > ${O}_single.log 2>&1; cat ${O}_single.log ;;
     perf) timeout 900 python scripts/perf.py time --shapes C1,C3,1x16k,C2,C4shard,C2fp8 > ${O}_perf.log 2>&1; cat ${O}_perf.log ;;
     *) echo "unknown recipe $r" >&2 ;;

@@ -257,16 +257,70 @@ CONFIGS = {
 }
 
 
+GRID_B = (1, 4, 16, 64, 256)
+GRID_S = (128, 512, 2048, 8192, 32768)
+HEADS = dict(num_q_heads=32, num_kv_heads=8, head_dim=128)
+
+
+def grid_shapes(kind):
+    """C5's batch x seq grid (ref: BASELINE.json configs[4]; Llama-3-8B heads), bounded so one pass
+    stays within minutes: prefill <= 2^19 tokens, decode <= 2^31 bytes of K+V."""
+    for b in GRID_B:
+        for s in GRID_S:
+            if kind == "prefill" and b * s > (1 << 19):
+                continue
+            if kind == "decode" and b * s * 8 * 128 * 2 * 2 > (1 << 31):
+                continue
+            yield f"{kind} b{b} s{s}", dict(op=kind, batch_size=b, seq_len=s, **HEADS, dtype="bfloat16", seed=0)
+
+
+def cdf(lines, comparators):
+    """relative_cdf (ref/pkg/src/ktune/report.py:196-230): per shape, ratio = library ms / ours ms
+    against the fastest of `comparators` on that shape; sorted ratios, mean, min, max, frac >= 1."""
+    by = {}
+    for ln in lines:
+        if "ms" in ln:
+            by.setdefault(ln["config"], {})[ln["impl"]] = ln["ms"]
+    ratios = []
+    for cfg, d in by.items():
+        ours = d.get("b200attn (ours)")
+        lib = [d[c] for c in comparators if c in d]
+        if ours and lib:
+            ratios.append((min(lib) / ours, cfg))
+    ratios.sort()
+    if not ratios:
+        return None
+    r = [x for x, _ in ratios]
+    return {"shapes": len(r), "mean": sum(r) / len(r), "min": r[0], "max": r[-1],
+            "frac_ge_1": sum(1 for x in r if x >= 1.0) / len(r), "ratios": [[round(x, 4), c] for x, c in ratios]}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="C1,C3,C2,C4_shard")
+    ap.add_argument("--grid", action="store_true", help="C5 grid: ours vs the trtllm-gen / cuDNN comparators")
     ap.add_argument("--n", type=int, default=10)
     ap.add_argument("--out", default="gpurun_out/sota.json")
     args = ap.parse_args()
     lines = []
-    for c in args.configs.split(","):
-        kind, shape = CONFIGS[c]
-        run(c, kind, shape, lines, args.n if c != "C1" else 20)
+    if args.grid:
+        global prefill_cases, decode_cases
+        keep_pf = ("flashinfer-trtllm-gen (fmhaSm100a)", "cudnn-sdpa (torch, per sequence)")
+        keep_dec = ("flashinfer-trtllm-gen decode (fmhaSm100a)",)
+        pf_all, dec_all = prefill_cases, decode_cases
+        prefill_cases = lambda x, sc: ((n, f) for n, f in pf_all(x, sc) if n in keep_pf)  # noqa: E731
+        decode_cases = lambda d, sc: ((n, f) for n, f in dec_all(d, sc) if n in keep_dec)  # noqa: E731
+        for kind in ("prefill", "decode"):
+            for name, shape in grid_shapes(kind):
+                run(name, kind, shape, lines, args.n)
+        summary = {"prefill": cdf([ln for ln in lines if ln["config"].startswith("prefill")], keep_pf),
+                   "decode": cdf([ln for ln in lines if ln["config"].startswith("decode")], keep_dec)}
+        print(json.dumps({"relative_cdf_vs_best_library": summary}), flush=True)
+        lines.append({"relative_cdf_vs_best_library": summary})
+    else:
+        for c in args.configs.split(","):
+            kind, shape = CONFIGS[c]
+            run(c, kind, shape, lines, args.n if c != "C1" else 20)
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)
     Path(args.out).write_text(json.dumps(lines, indent=1))
 
