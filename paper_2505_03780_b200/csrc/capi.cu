@@ -40,7 +40,7 @@ constexpr int kNumSMs = 148;
 // Every decode workspace starts with kFlatCounters int32 arrival counters (K2' in-kernel merge) at a
 // FIXED offset, so launches of different shapes / kernels sharing one workspace never read each
 // other's partials as counters (zero before first use; every launch leaves them zero).
-constexpr size_t kFlatCounters = 1024;  // == FlatCfg::MAXB
+constexpr size_t kFlatCounters = 1024;  // batches above this use the K3' combine (no fused merge)
 
 thread_local char g_err[512] = "";
 
@@ -352,7 +352,8 @@ const DecodeEntry kDecode[] = {DF(2), DF(3), DF(4), DF(5), DF(6)};
 #undef DF
 
 
-// ---- K2' flat partition (TILE_N = 16: one page of all 8 kv heads per MMA tile)
+// ---- K2' flat partition (TILE_N = 16: 16-token page chunks of all kv heads, 128 (chunk, head,
+// token) rows per MMA tile)
 int num_sms() {  // per device (cached; a process may drive several GPUs)
   static std::atomic<int> cache[kMaxDevices];
   int dev = 0;
@@ -386,18 +387,22 @@ bool flat_fused_merge(int batch, int ctas) {
     const char* e = getenv("B200ATTN_FLAT_MERGE");
     force = (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : -1;
   }
+  if (batch > (int)kFlatCounters) return false;  // the arrival counters cover the first 1024 sequences
   if (force >= 0) return force == 1;
   return ctas <= 8 * batch;
 }
 
 using FlatLauncher = int (*)(const b200attn_decode_params*, bool combine, cudaStream_t);
 
-template <int G, int NS, bool FP8>
+template <int HKV, int G, int NS, bool FP8>
 int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stream) {
-  using C = b200::FlatCfg<G, NS, FP8>;
-  auto kern = b200::decode_flat_kernel<G, NS, FP8>;
-  if (int rc0 = ensure_smem_attr(reinterpret_cast<const void*>(kern), C::SMEM_BYTES,
-                               "cudaFuncSetAttribute(decode_flat)"))
+  using C = b200::FlatCfg<HKV, G, NS, FP8>;
+  auto kern = b200::decode_flat_kernel<HKV, G, NS, FP8>;
+  // the per-sequence tile prefix lives in smem: the launch's dynamic size grows with the batch
+  const int smem = C::smem_bytes(p->batch);
+  if (smem > kMaxSmem)
+    return fail(B200ATTN_SMEM_OVERFLOW, "decode_flat: batch %d needs %d B smem > %d", p->batch, smem, kMaxSmem);
+  if (int rc0 = ensure_smem_attr(reinterpret_cast<const void*>(kern), kMaxSmem, "cudaFuncSetAttribute(decode_flat)"))
     return rc0;
   const int D = 128;
   CUtensorMap mq, mk, mv;
@@ -407,12 +412,12 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
     return rc;
   // head-major view of the page pool: dims {d, token, head}, strides {Hkv*D*2, D*2} (transposed)
   const uint64_t tokens = (uint64_t)p->num_blocks * p->block_size;
-  if (FP8) {  // one {128 d, 16 tokens, 8 heads} byte box = the whole 16-KB page
-    if ((rc = make_map_u8_3d(&mk, p->k_cache, D, tokens, 8, 8ull * D, D, D, C::TT, 8))) return rc;
-    if ((rc = make_map_u8_3d(&mv, p->v_cache, D, tokens, 8, 8ull * D, D, D, C::TT, 8))) return rc;
+  if (FP8) {  // one {128 d, 16 tokens, Hkv heads} byte box = a whole 16-token chunk (16 KB at Hkv = 8)
+    if ((rc = make_map_u8_3d(&mk, p->k_cache, D, tokens, HKV, (uint64_t)HKV * D, D, D, 16, HKV))) return rc;
+    if ((rc = make_map_u8_3d(&mv, p->v_cache, D, tokens, HKV, (uint64_t)HKV * D, D, D, 16, HKV))) return rc;
   } else {
-    if ((rc = make_map_3d(&mk, p->k_cache, D, tokens, 8, 8ull * D * 2, D * 2ull, C::TT, 8))) return rc;
-    if ((rc = make_map_3d(&mv, p->v_cache, D, tokens, 8, 8ull * D * 2, D * 2ull, C::TT, 8))) return rc;
+    if ((rc = make_map_3d(&mk, p->k_cache, D, tokens, HKV, (uint64_t)HKV * D * 2, D * 2ull, 16, HKV))) return rc;
+    if ((rc = make_map_3d(&mv, p->v_cache, D, tokens, HKV, (uint64_t)HKV * D * 2, D * 2ull, 16, HKV))) return rc;
   }
   // persistent CTAs, but at least kFlatMinTiles tiles each when the (host-known upper bound of
   // the) tile count is small: fewer partial segments to merge, same memory parallelism
@@ -440,7 +445,7 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
     a.scale_log2 *= (p->k_scale > 0.f ? p->k_scale : 1.f);
     a.out_scale = (p->v_scale > 0.f ? p->v_scale : 1.f);
   }
-  kern<<<ctas, C::NTHREADS, C::SMEM_BYTES, stream>>>(mq, mk, mv, a);
+  kern<<<ctas, C::NTHREADS, smem, stream>>>(mq, mk, mv, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "decode_flat launch");
   if (combine && !fused) {
@@ -453,18 +458,25 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
 }
 
 struct FlatEntry {
-  int g, ns;
+  int hkv, g, ns;
   bool fp8;
   FlatLauncher fn;
-  int smem;
+  int smem;  // at batch 1024
 };
-#define FF(G, NS) {G, NS, false, &launch_flat<G, NS, false>, b200::FlatCfg<G, NS, false>::SMEM_BYTES}
-#define F8(G, NS) {G, NS, true, &launch_flat<G, NS, true>, b200::FlatCfg<G, NS, true>::SMEM_BYTES}
-const FlatEntry kFlat[] = {FF(1, 3), FF(1, 4), FF(1, 5), FF(1, 6), FF(2, 3), FF(2, 4), FF(2, 5), FF(2, 6),
-                           FF(4, 3), FF(4, 4), FF(4, 5), FF(8, 3), FF(8, 4),
-                           // fp8 e4m3 KV: num_stages = depth of the ring of 16-KB pages
-                           F8(1, 4), F8(1, 6), F8(1, 8), F8(2, 4), F8(2, 6), F8(2, 8), F8(4, 4), F8(4, 6),
-                           F8(4, 8), F8(8, 4), F8(8, 6)};
+#define FF(H, G, NS) {H, G, NS, false, &launch_flat<H, G, NS, false>, b200::FlatCfg<H, G, NS, false>::SMEM_BYTES}
+#define F8(H, G, NS) {H, G, NS, true, &launch_flat<H, G, NS, true>, b200::FlatCfg<H, G, NS, true>::SMEM_BYTES}
+const FlatEntry kFlat[] = {FF(8, 1, 3), FF(8, 1, 4), FF(8, 1, 5), FF(8, 1, 6), FF(8, 2, 3), FF(8, 2, 4),
+                           FF(8, 2, 5), FF(8, 2, 6), FF(8, 4, 3), FF(8, 4, 4), FF(8, 4, 5), FF(8, 8, 3),
+                           FF(8, 8, 4),
+                           // Hkv = 1 / 2 / 4 (kv-head shards of GQA models, or such models outright):
+                           // PPT = 8 / Hkv page chunks per 128-row tile
+                           FF(4, 1, 4), FF(4, 2, 4), FF(4, 4, 4), FF(4, 8, 4), FF(4, 2, 5), FF(4, 4, 5),
+                           FF(2, 1, 4), FF(2, 2, 4), FF(2, 4, 4), FF(2, 8, 4), FF(2, 4, 5), FF(2, 8, 5),
+                           FF(1, 1, 4), FF(1, 2, 4), FF(1, 4, 4), FF(1, 8, 4), FF(1, 8, 5),
+                           // fp8 e4m3 KV: num_stages = depth of the ring of 16-KB tiles
+                           F8(8, 1, 4), F8(8, 1, 6), F8(8, 1, 8), F8(8, 2, 4), F8(8, 2, 6), F8(8, 2, 8),
+                           F8(8, 4, 4), F8(8, 4, 6), F8(8, 4, 8), F8(8, 8, 4), F8(8, 8, 6), F8(4, 2, 8),
+                           F8(4, 4, 8), F8(4, 8, 6), F8(2, 4, 8), F8(2, 8, 6), F8(1, 8, 8)};
 #undef FF
 #undef F8
 
@@ -473,30 +485,33 @@ int check_flat(const b200attn_decode_params* p, const b200attn_decode_variant* v
     return fail(B200ATTN_UNSUPPORTED_CONFIG,
                 "num_splits=%d: TILE_N=16 uses the flat stream partition (one CTA per SM); num_splits must be 0",
                 v->num_splits);
-  if (p->num_kv_heads != 8)
-    return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16 packs 8 kv heads x 16 tokens per tile; num_kv_heads=%d",
-                p->num_kv_heads);
+  const int H = p->num_kv_heads;
+  if (H != 1 && H != 2 && H != 4 && H != 8)
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16 packs 1/2/4/8 kv heads per 16-token chunk; num_kv_heads=%d",
+                H);
   const int G = p->num_q_heads / p->num_kv_heads;
   if (G != 1 && G != 2 && G != 4 && G != 8)
     return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16 compiled for GQA groups 1/2/4/8, got %d", G);
-  if (p->block_size < 16)
-    return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16 needs block_size >= 16, got %d", p->block_size);
-  if (p->batch > b200::FlatCfg<1, 3>::MAXB)
-    return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16 supports batch <= %d", b200::FlatCfg<1, 3>::MAXB);
+  if (p->block_size < 16 || (p->block_size & (p->block_size - 1)))
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16 needs a power-of-two block_size >= 16, got %d",
+                p->block_size);
   const bool fp8 = p->kv_dtype == B200ATTN_KV_FP8_E4M3;
   const FlatEntry* e = nullptr;
   for (const auto& x : kFlat)
-    if (x.g == G && x.ns == v->num_stages && x.fp8 == fp8) e = &x;
+    if (x.hkv == H && x.g == G && x.ns == v->num_stages && x.fp8 == fp8) e = &x;
   if (!e) {
     const int np = 8 * G < 16 ? 16 : 8 * G;
     const int est = v->num_stages * 32768 + 4 * np * 256 + 4096 + 1024;
     if (est > kMaxSmem)
       return fail(B200ATTN_SMEM_OVERFLOW, "TILE_N=16 num_stages=%d with %d q heads needs ~%d B smem > %d",
                   v->num_stages, p->num_q_heads, est, kMaxSmem);
-    return fail(B200ATTN_UNSUPPORTED_CONFIG, "TILE_N=16: no compiled %s variant for num_stages=%d with GQA %d",
-                fp8 ? "fp8" : "bf16", v->num_stages, G);
+    return fail(B200ATTN_UNSUPPORTED_CONFIG,
+                "TILE_N=16: no compiled %s variant for num_stages=%d with %d kv heads x GQA %d", fp8 ? "fp8" : "bf16",
+                v->num_stages, H, G);
   }
-  if (e->smem > kMaxSmem) return fail(B200ATTN_SMEM_OVERFLOW, "decode_flat smem %d B", e->smem);
+  const int smem = e->smem + (p->batch - 1024) * 4;  // the cu array is sized per batch
+  if (smem > kMaxSmem)
+    return fail(B200ATTN_SMEM_OVERFLOW, "decode_flat: batch %d needs %d B smem > %d", p->batch, smem, kMaxSmem);
   *out = e;
   return B200ATTN_OK;
 }

@@ -1,12 +1,14 @@
 // decode_flat_sm100.cuh — K2': paged-KV decode, flat (stream-K style) partition, all KV heads
-// per CTA, sm_100a.   Selected by TILE_N = 16 (tokens per MMA tile).
+// per CTA, sm_100a.   Selected by TILE_N = 16 (tokens per page chunk).
 //
-// Why: a page of the vLLM cache [num_blocks, bs, Hkv=8, 128] holds 16 tokens x 8 heads = 32 KB
-// contiguous.  K2 (decode_sm100.cuh) gathers it per kv head as 2-KB strided boxes; here one
-// TMA box {64 d, 16 tokens, 8 heads} per 64-column half moves the whole page, and the MMA M
-// dimension is the page's 128 (head, token) rows.  The tensor map is head-major (strides
-// {2048 B token, 256 B head} — transposed) so smem row r = head*16 + token: every warp owns
-// two heads, the per-head max over the tile is a 16-lane shuffle and nothing crosses warps.
+// Why: 16 tokens of a page of the vLLM cache [num_blocks, bs, Hkv, 128] hold 16 x Hkv x 256 B
+// contiguous (32 KB at Hkv = 8).  K2 (decode_sm100.cuh) gathers it per kv head as 2-KB strided
+// boxes; here one TMA box {64 d, 16 tokens, Hkv heads} per 64-column half moves the whole chunk,
+// and the MMA M dimension is 128 (chunk, head, token) rows: one chunk at Hkv = 8, PPT = 8 / Hkv
+// chunks (TT = 128 / Hkv tokens) at Hkv = 1, 2, 4.  The tensor map is head-major (strides
+// {Hkv*256 B token, 256 B head} — transposed) so smem row r = (chunk*Hkv + head)*16 + token: every
+// 16-row group is one (chunk, head), every warp owns two groups; the per-head max over a tile is a
+// 16-lane shuffle (plus, at Hkv < 8, a max over the PPT groups of the head through smem).
 //
 //   S^T[(h,t), qh] = K_page[(h,t), :] . Q[qh, :]^T            M=128 rows, N = Hq (pad 16)
 //   O^T[d, qh]    += V_page^T[d, (h,t)] . P^T[(h,t), qh]       P^T block-diagonal: entries with
@@ -47,10 +49,14 @@ struct FlatDecodeArgs {
   float out_scale;   // 1                        (fp8: v_scale)
 };
 
-template <int G, int NSTAGE, bool FP8 = false>
+template <int HKV_, int G, int NSTAGE, bool FP8 = false>
 struct FlatCfg {
-  static constexpr int D = 128, HKV = 8, TT = 16, ROWS = 128;
-  static constexpr int NQ = 8 * G;
+  static constexpr int D = 128, HKV = HKV_, ROWS = 128;
+  static constexpr int TT = ROWS / HKV;  // tokens per MMA tile
+  static constexpr int PPT = TT / 16;    // 16-token page chunks per tile (one TMA box pair each)
+  static constexpr int NQ = HKV * G;
+  static_assert(HKV == 1 || HKV == 2 || HKV == 4 || HKV == 8, "Hkv in {1,2,4,8}");
+  static_assert(!FP8 || NQ >= 8, "fp8 Q split: at least 8 q heads (16 threads per q head)");
   static constexpr int NP = NQ < 16 ? 16 : NQ;  // MMA N per operand term
   static constexpr int NT = FP8 ? 2 : 1;        // terms stacked along N (hi, lo)
   static constexpr int NTHREADS = 192, TMA_WARP = 4, MMA_WARP = 5;
@@ -58,7 +64,6 @@ struct FlatCfg {
   static constexpr int QB = NP * 256, QHALF = NP * 128;  // bf16 Q tile (as TMA loads it)
   static constexpr int Q8B = 2 * NP * 128;               // fp8 [Q_hi; Q_lo] tile (FP8)
   static constexpr int PB = FP8 ? 2 * NP * 128 : NP * 256, PHALF = NP * 128;
-  static constexpr int MAXB = 1024;
   static constexpr int OFF_KV = 0;
   static constexpr int OFF_Q = OFF_KV + NSTAGE * SLOT;
   static constexpr int OFF_Q8 = OFF_Q + 2 * QB;
@@ -66,15 +71,21 @@ struct FlatCfg {
   static constexpr int OFF_ALPHA = OFF_P + 2 * PB;       // [NP] f32 rescale factors + int32 flags[2][4]
   static constexpr int OFF_QS = OFF_ALPHA + 2 * NP * 4;  // [2][NP] f32 per-q-head Q scales (FP8)
   static constexpr int OFF_ML = OFF_QS + 2 * NP * 4;     // [2][NP] f32
-  static constexpr int OFF_CU = OFF_ML + 2 * NP * 4;     // [MAXB + 1] i32
-  static constexpr int OFF_BAR = (OFF_CU + (MAXB + 1) * 4 + 7) & ~7;
+  static constexpr int OFF_GRP = OFF_ML + 2 * NP * 4;    // [8][G] f32 per-(chunk, head) max / sum (HKV < 8)
+  static constexpr int OFF_BAR = (OFF_GRP + 8 * G * 4 + 7) & ~7;
   static constexpr int NUM_BARS = 4 + 2 * NSTAGE + 8 + 2;
-  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  static constexpr int OFF_CU = OFF_BAR + NUM_BARS * 8 + 16;  // [batch + 1] i32 (sized per launch)
+  // dynamic smem of a launch: the cu array grows with the batch (+1024 for the base alignment)
+  __host__ __device__ static constexpr int smem_bytes(int batch) { return OFF_CU + (batch + 1) * 4 + 1024; }
+  static constexpr int SMEM_BYTES = smem_bytes(1024);  // nominal (the dispatcher's size check)
   static constexpr int TCOLS = 4 * NT * NP;  // S[2] + O[2], NT terms each
   static constexpr uint32_t TMEM_COLS = TCOLS <= 64 ? 64 : (TCOLS <= 128 ? 128 : (TCOLS <= 256 ? 256 : 512));
   __host__ __device__ static constexpr uint32_t S_COL(int i) { return (i & 1) * NT * NP; }                // per tile
   __host__ __device__ static constexpr uint32_t O_COL(int k) { return 2 * NT * NP + (k & 1) * NT * NP; }  // per segment
   static constexpr float LAZY = FP8 ? 4.0f : 8.0f;  // log2 headroom before the running max moves
+  // a warp's two 16-row groups hold heads (2w) % HKV and (2w + 1) % HKV: adjacent S column ranges
+  // (2 G columns) at HKV >= 2, the same range (G columns) at HKV = 1
+  static constexpr int WCOLS = HKV >= 2 ? 2 * G : G;
 };
 
 __device__ __forceinline__ int flat_cta_of(int t, int ctas, int ntiles) {
@@ -196,12 +207,12 @@ __device__ __forceinline__ void flat_merge_if_last(const FlatDecodeArgs& args, c
   }
 }
 
-template <int G, int NSTAGE, bool FP8 = false>
-__global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
+template <int HKV, int G, int NSTAGE, bool FP8 = false>
+__global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
     decode_flat_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
                        const __grid_constant__ CUtensorMap tmap_v, const FlatDecodeArgs args) {
-  using C = FlatCfg<G, NSTAGE, FP8>;
-  constexpr int NQ = C::NQ, NP = C::NP, D = C::D, NT = C::NT;
+  using C = FlatCfg<HKV, G, NSTAGE, FP8>;
+  constexpr int NQ = C::NQ, NP = C::NP, D = C::D, NT = C::NT, PPT = C::PPT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sKV = smem + C::OFF_KV;
@@ -211,6 +222,7 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
   float* alpha_s = reinterpret_cast<float*>(smem + C::OFF_ALPHA);
   float* qs_s = reinterpret_cast<float*>(smem + C::OFF_QS);
   float* ml_s = reinterpret_cast<float*>(smem + C::OFF_ML);
+  float* grp_s = reinterpret_cast<float*>(smem + C::OFF_GRP);
   int32_t* cu = reinterpret_cast<int32_t*>(smem + C::OFF_CU);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars;       // [2] bf16 Q landed (TMA)
@@ -226,20 +238,28 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
   const int warp = warp_id(), lane = lane_id();
   const int B = args.batch;
 
-  // ---- tiles per sequence -> cu (exclusive prefix), one warp
-  if (warp == 0) {
-    int carry = 0;
-    if (lane == 0) cu[0] = 0;
-    for (int base = 0; base < B; base += 32) {
-      const int b = base + lane;
-      int v = b < B ? (args.seq_lens[b] + C::TT - 1) / C::TT : 0;
+  // ---- tiles per sequence -> cu (exclusive prefix), block-wide: each thread scans a contiguous
+  // chunk of sequences (any batch size, no serial chain of loads)
+  {
+    __shared__ int warp_tot[C::NTHREADS / 32];
+    const int per = (B + C::NTHREADS - 1) / C::NTHREADS;
+    const int b0 = min(B, static_cast<int>(threadIdx.x) * per), b1 = min(B, b0 + per);
+    int local = 0;
+    for (int b = b0; b < b1; ++b) local += (args.seq_lens[b] + C::TT - 1) / C::TT;
+    int incl = local;
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int n = __shfl_up_sync(0xffffffffu, v, off);
-        if (lane >= off) v += n;
-      }
-      if (b < B) cu[b + 1] = carry + v;
-      carry += __shfl_sync(0xffffffffu, v, 31);
+    for (int off = 1; off < 32; off <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += n;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    int run = incl - local;
+    for (int w = 0; w < warp; ++w) run += warp_tot[w];
+    if (threadIdx.x == 0) cu[0] = 0;
+    for (int b = b0; b < b1; ++b) {
+      run += (args.seq_lens[b] + C::TT - 1) / C::TT;
+      cu[b + 1] = run;
     }
   }
   // zero Q (padded rows), the fp8 Q split and P^T (block-diagonal zeros) once
@@ -307,6 +327,7 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
       while (cu[b + 1] <= t) ++b;
       const int seg_end = min(T1, cu[b + 1]);
       const int tile0 = cu[b];
+      const int len = args.seq_lens[b];
       if (lane == 0) {
         mbar_wait(&q_empty[k & 1], ((k >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&q_full[k & 1], 2 * NQ * 128);
@@ -314,24 +335,34 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
           tma_load_3d(sQ + (k & 1) * C::QB + hf * C::QHALF, &tmap_q, &q_full[k & 1], hf * 64, 0, b);
       }
       const int32_t* bt = args.block_table + static_cast<size_t>(b) * args.max_blocks;
-      for (int base = t; base < seg_end; base += 32) {
-        const int n = min(32, seg_end - base);
+      // 16-token page chunks, 32 per warp load of the block table (PPT per tile); chunks past the
+      // sequence end (last tile at Hkv < 8) reload its first chunk — masked by the softmax
+      auto chunk_tok = [&](int ci) { return ci * 16 < len ? ci * 16 : 0; };
+      constexpr int TPB = 32 / PPT;  // tiles per block-table load
+      for (int base = t; base < seg_end; base += TPB) {
+        const int n = min(TPB, seg_end - base);
         int page = 0;
-        if (lane < n) page = __ldg(bt + ((base + lane - tile0) * C::TT) / bs);
+        if (lane < n * PPT) page = __ldg(bt + chunk_tok((base - tile0) * PPT + lane) / bs);
         for (int j = 0; j < n; ++j) {
-          const int pg = __shfl_sync(0xffffffffu, page, j);
-          const int tok = (base + j - tile0) * C::TT;
-          const int row = pg * bs + (tok & (bs - 1));
-          if (lane == 0) {
 #pragma unroll
-            for (int kv = 0; kv < 2; ++kv, ++it) {
-              const int slot = it % NSTAGE;
+          for (int kv = 0; kv < 2; ++kv, ++it) {
+            const int slot = it % NSTAGE;
+            uint8_t* dst = sKV + slot * C::SLOT;
+            const CUtensorMap* map = kv ? &tmap_v : &tmap_k;
+            if (lane == 0) {
               mbar_wait(&kv_empty[slot], ((it / NSTAGE) & 1) ^ 1);
               mbar_arrive_expect_tx(&kv_full[slot], C::SLOT);
-              uint8_t* dst = sKV + slot * C::SLOT;
-              const CUtensorMap* map = kv ? &tmap_v : &tmap_k;
-              tma_load_3d_hint(dst, map, &kv_full[slot], 0, row, 0, stream_once);
-              if (!FP8) tma_load_3d_hint(dst + C::HALF, map, &kv_full[slot], 64, row, 0, stream_once);
+            }
+#pragma unroll
+            for (int pc = 0; pc < PPT; ++pc) {
+              const int pg = __shfl_sync(0xffffffffu, page, j * PPT + pc);
+              const int tok = chunk_tok((base + j - tile0) * PPT + pc);
+              const int row = pg * bs + (tok & (bs - 1));
+              if (lane == 0) {
+                uint8_t* d = dst + pc * 16 * HKV * 128;  // rows (chunk, head, token) of 128 B per half
+                tma_load_3d_hint(d, map, &kv_full[slot], 0, row, 0, stream_once);
+                if (!FP8) tma_load_3d_hint(d + C::HALF, map, &kv_full[slot], 64, row, 0, stream_once);
+              }
             }
           }
         }
@@ -409,11 +440,12 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
     // FA4's lazy rescale): then, and on a segment's first tile, the CTA takes the slow path —
     // exact per-head max (16-lane shuffles), alpha to smem, and once PV(i-1) has landed every
     // thread rescales its O^T row in TMEM.  The common tile is a vote, G exp2 and G P stores.
-    const int row = threadIdx.x;  // S^T row (head*16 + token) and O^T row (d)
-    const int h = row >> 4, t16 = row & 15;
+    const int row = threadIdx.x;  // S^T row ((chunk*Hkv + head)*16 + token) and O^T row (d)
+    const int grp = row >> 4, t16 = row & 15;
+    const int h = grp % HKV, pch = grp / HKV;  // kv head, page chunk within the tile
     const bool upper = (lane >> 4) != 0;
     const uint32_t lane_base = static_cast<uint32_t>(warp << 5) << 16;
-    const uint32_t col_base = static_cast<uint32_t>(warp * 2 * G);
+    const uint32_t col_base = static_cast<uint32_t>(((2 * warp) % HKV) * G);
     const float sl2 = args.scale_log2;
     const uint32_t p_base = smem_u32(sP) + (row >> 6) * C::PHALF + (row & 7) * 2;  // bf16 P^T
     const int rchunk = (row & 63) >> 3;
@@ -485,25 +517,29 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
       for (; t < seg_end; ++t, ++i) {
         const int sb = i & 1;
         mbar_wait(&s_full[sb], (i >> 1) & 1);
+        // observe every phase of o_full (compute-sanitizer synccheck): PV(i-2) was issued before
+        // QK(i) and tcgen05 ops complete in order, so this wait returns at once
+        if (i >= 2) mbar_wait(&o_full[(i - 2) & 1], ((i - 2) >> 1) & 1);
         tc_fence_after();
-        const int tok = (t - tile0) * C::TT + t16;
+        const int tok = (t - tile0) * C::TT + pch * 16 + t16;
         const bool valid = tok < len;
         float x[G];
         bool need = false;
         {
-          uint32_t sv[2 * G];
-          tmem_ld_cols<2 * G>(tmem + lane_base + C::S_COL(i) + col_base, sv);
+          constexpr int WC = C::WCOLS, UO = WC - G;  // upper half-warp's column offset (0 at Hkv = 1)
+          uint32_t sv[WC];
+          tmem_ld_cols<WC>(tmem + lane_base + C::S_COL(i) + col_base, sv);
           if constexpr (FP8) {
-            uint32_t sl[2 * G];
-            tmem_ld_cols<2 * G>(tmem + lane_base + C::S_COL(i) + NP + col_base, sl);
+            uint32_t sl[WC];
+            tmem_ld_cols<WC>(tmem + lane_base + C::S_COL(i) + NP + col_base, sl);
 #pragma unroll
             for (int g = 0; g < G; ++g)
-              x[g] = valid ? fmaf(__uint_as_float(upper ? sl[G + g] : sl[g]), 0.0625f,
-                                  __uint_as_float(upper ? sv[G + g] : sv[g])) * fac[g]
+              x[g] = valid ? fmaf(__uint_as_float(upper ? sl[UO + g] : sl[g]), 0.0625f,
+                                  __uint_as_float(upper ? sv[UO + g] : sv[g])) * fac[g]
                            : -INFINITY;
           } else {
 #pragma unroll
-            for (int g = 0; g < G; ++g) x[g] = valid ? __uint_as_float(upper ? sv[G + g] : sv[g]) * fac[g] : -INFINITY;
+            for (int g = 0; g < G; ++g) x[g] = valid ? __uint_as_float(upper ? sv[UO + g] : sv[g]) * fac[g] : -INFINITY;
           }
         }
 #pragma unroll
@@ -513,11 +549,30 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
         named_bar_sync(1, 128);
         if (flags[sb * 4 + 0] | flags[sb * 4 + 1] | flags[sb * 4 + 2] | flags[sb * 4 + 3]) {
           // slow path (CTA-uniform): exact head maxima, rescale factors, O rescale
+          float mts[G];
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             float mt = x[g];
 #pragma unroll
             for (int off = 1; off < 16; off <<= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
+            mts[g] = mt;
+          }
+          if constexpr (PPT > 1) {  // a head spans PPT 16-row groups (one per page chunk)
+            if (t16 == 0)
+#pragma unroll
+              for (int g = 0; g < G; ++g) grp_s[grp * G + g] = mts[g];
+            named_bar_sync(1, 128);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              float m = grp_s[h * G + g];
+#pragma unroll
+              for (int pc = 1; pc < PPT; ++pc) m = fmaxf(m, grp_s[(pc * HKV + h) * G + g]);
+              mts[g] = m;
+            }
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float mt = mts[g];
             float alpha = 1.f;
             if (mt > m_run[g] + LAZY) {
               alpha = (m_run[g] == -INFINITY) ? 0.f : fast_exp2(m_run[g] - mt);
@@ -595,14 +650,32 @@ __global__ void __launch_bounds__(FlatCfg<G, NSTAGE, FP8>::NTHREADS, 1)
       }
 
       // ---- segment epilogue: O^T (TMEM) / l, or the unnormalised partial for K3'
+      float lg[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         float l = l_part[g];
 #pragma unroll
         for (int off = 1; off < 16; off <<= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-        if (t16 == 0) {
+        lg[g] = l;
+      }
+      if constexpr (PPT > 1) {  // sum the head's PPT groups
+        if (t16 == 0)
+#pragma unroll
+          for (int g = 0; g < G; ++g) grp_s[grp * G + g] = lg[g];
+        named_bar_sync(1, 128);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          float l = grp_s[h * G + g];
+#pragma unroll
+          for (int pc = 1; pc < PPT; ++pc) l += grp_s[(pc * HKV + h) * G + g];
+          lg[g] = l;
+        }
+      }
+      if (t16 == 0 && pch == 0) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
           ml_s[h * G + g] = m_run[g];
-          ml_s[NP + h * G + g] = l;
+          ml_s[NP + h * G + g] = lg[g];
         }
       }
       // last PV of this segment (in-order completion: every earlier PV has landed too).  Per-parity

@@ -545,6 +545,9 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
       for (int j = 0; j < n_kv; ++j) {
         const int buf = (gt + j) % C::SB;
         mbar_wait(&s_full[t * C::SB + buf], ((gt + j) / C::SB) & 1);
+        // observe every phase of o_done (compute-sanitizer synccheck): PV_t(g - LA) was issued before
+        // QK_t(g) and tcgen05 ops complete in order, so this wait returns at once
+        if (gt + j >= C::LA) mbar_wait(&o_done[2 * t + ((gt + j - C::LA) & 1)], ((gt + j - C::LA) >> 1) & 1);
         tc_fence_after();
         const uint32_t s_addr = s_base + C::S_COL(t, buf);
         if (row == 0 && hh == 0) TRACE(t, gt + j);

@@ -319,6 +319,14 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 
 // TMEM -> registers, 32 lanes x 32b, 16 / 32 consecutive columns per thread.
 // The wait::ld is fused into the same asm so no consumer can be hoisted above it.
+__device__ __forceinline__ void tmem_ld1(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0])
+      : "r"(taddr)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld2(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n\t"
@@ -366,10 +374,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr)
       : "memory");
 }
-// N consecutive fp32 columns (N in {2,4,8,16,32,64,...}) into r[0..N)
+// N consecutive fp32 columns (N in {1,2,4,8,16,32,64,...}) into r[0..N)
 template <int N>
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
-  if constexpr (N == 2) {
+  if constexpr (N == 1) {
+    tmem_ld1(taddr, r);
+  } else if constexpr (N == 2) {
     tmem_ld2(taddr, r);
   } else if constexpr (N == 4) {
     tmem_ld4(taddr, r);
@@ -408,10 +418,27 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
 }
-// N consecutive fp32 columns (N in {8, 16, 32, 64, ...}) from r[0..N)
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(r[0]) : "memory");
+}
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(r[0]), "r"(r[1]) : "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3])
+               : "memory");
+}
+// N consecutive fp32 columns (N in {1, 2, 4, 8, 16, 32, 64, ...}) from r[0..N)
 template <int N>
 __device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t* r) {
-  if constexpr (N == 8) {
+  if constexpr (N == 1) {
+    tmem_st1(taddr, r);
+  } else if constexpr (N == 2) {
+    tmem_st2(taddr, r);
+  } else if constexpr (N == 4) {
+    tmem_st4(taddr, r);
+  } else if constexpr (N == 8) {
     tmem_st8(taddr, r);
   } else if constexpr (N == 16) {
     tmem_st16(taddr, *reinterpret_cast<const uint32_t(*)[16]>(r));

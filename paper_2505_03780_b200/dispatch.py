@@ -26,12 +26,16 @@ PREFILL_DEFAULT = {"BLOCK_M": 256, "BLOCK_N": 128, "num_warps": 4, "num_stages":
                    "PRE_LOAD_V": False}
 PREFILL_FIXED_BASELINE = {"BLOCK_M": 128, "BLOCK_N": 128, "num_warps": 4, "num_stages": 2, "waves_per_eu": 1,
                           "PRE_LOAD_V": False}
-DECODE_DEFAULT = {"num_splits": 0, "num_stages": 5, "TILE_N": 16}  # flat partition, 8 kv heads per tile
+DECODE_DEFAULT = {"num_splits": 0, "num_stages": 5, "TILE_N": 16}  # flat partition, all kv heads per tile
 DECODE_SPLIT_DEFAULT = {"num_splits": 0, "num_stages": 4, "TILE_N": 128}  # any geometry
 
 _GEOM = ("num_q_heads", "num_kv_heads", "head_dim", "block_size", "causal", "kv_dtype")
-# fp8 KV (TILE_N=16 only): num_stages = depth of the ring of 16-KB pages; deepest compiled variant per GQA group
-FP8_DECODE_STAGES = {1: 8, 2: 8, 4: 8, 8: 6}
+# fp8 KV (TILE_N=16 only): num_stages = depth of the ring of 16-KB tiles; deepest compiled variant per
+# (kv heads, GQA group) — capi.cu kFlat
+FP8_DECODE_STAGES = {(8, 1): 8, (8, 2): 8, (8, 4): 8, (8, 8): 6, (4, 2): 8, (4, 4): 8, (4, 8): 6, (2, 4): 8,
+                     (2, 8): 6, (1, 8): 8}
+# bf16 flat kernels at Hkv < 8 (kv-head shards): ring depth compiled for every GQA group
+FLAT_STAGES_NARROW = 4
 
 _table = None
 
@@ -161,24 +165,32 @@ def default_prefill_config(**dims) -> dict:
     return dict(cfg)
 
 
+FLAT_MAX_BATCH = 8192  # the flat kernel keeps the per-sequence tile prefix in smem (4 B per sequence)
+
+
 def flat_decode_ok(num_q_heads=32, num_kv_heads=8, block_size=16, batch_size=1, **_) -> bool:
-    """Shapes the TILE_N=16 flat-partition kernel is compiled for (else the per-head split kernel)."""
-    return (num_kv_heads == 8 and num_q_heads // num_kv_heads in (1, 2, 4, 8) and num_q_heads % 8 == 0
-            and block_size >= 16 and batch_size <= 1024)
+    """Shapes the TILE_N=16 flat-partition kernel is compiled for (else the per-head split kernel):
+    1/2/4/8 kv heads x GQA 1/2/4/8, power-of-two pages of >= 16 tokens."""
+    return (num_kv_heads in (1, 2, 4, 8) and num_q_heads % num_kv_heads == 0
+            and num_q_heads // num_kv_heads in (1, 2, 4, 8)
+            and block_size >= 16 and block_size & (block_size - 1) == 0 and batch_size <= FLAT_MAX_BATCH)
 
 
 def default_decode_config(**dims) -> dict:
+    Hkv = max(dims.get("num_kv_heads", 8), 1)
+    G = dims.get("num_q_heads", 32) // Hkv
     if str(dims.get("kv_dtype", "bfloat16")).startswith(("fp8", "float8")):
         cfg = lookup("decode", dims)
-        G = dims.get("num_q_heads", 32) // max(dims.get("num_kv_heads", 8), 1)
         if cfg is None or cfg.get("TILE_N") != 16:
-            cfg = {"num_splits": 0, "num_stages": FP8_DECODE_STAGES.get(G, 4), "TILE_N": 16}
+            cfg = {"num_splits": 0, "num_stages": FP8_DECODE_STAGES.get((Hkv, G), 4), "TILE_N": 16}
         return dict(cfg)
     cfg = lookup("decode", dims)
     if cfg is None:
         cfg = DECODE_DEFAULT if flat_decode_ok(**dims) else DECODE_SPLIT_DEFAULT
     if cfg.get("TILE_N") == 16 and not flat_decode_ok(**dims):
         cfg = DECODE_SPLIT_DEFAULT
-    if cfg.get("TILE_N") == 16 and dims.get("num_q_heads", 32) // 8 == 8 and cfg.get("num_stages", 4) > 4:
+    if cfg.get("TILE_N") == 16 and Hkv < 8:
+        cfg = dict(cfg, num_stages=FLAT_STAGES_NARROW)
+    if cfg.get("TILE_N") == 16 and Hkv * G == 64 and cfg.get("num_stages", 4) > 4:
         cfg = dict(cfg, num_stages=4)  # 64 q heads: Q/P buffers leave room for 4 ring slots
     return dict(cfg)

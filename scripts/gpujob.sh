@@ -13,6 +13,7 @@
 #   sota       scripts/sota.py (same-box library comparators)   single    single-launch vs amortised
 #   sotagrid   scripts/sota.py --grid (C5 grid, relative_cdf vs the best library per shape)
 #   perf       scripts/perf.py time over the BASELINE shapes
+#   narrow     K2' vs K2 on kv-head shards (Hkv = 1/2/4) and batch 4096     e2e   perf.py e2e breakdown
 set -u
 TAG=$1; shift
 mkdir -p gpurun_out
@@ -45,6 +46,10 @@ for r in "$@"; do
     sotagrid) timeout 2400 python scripts/sota.py --grid --out ${O}_sotagrid.json > ${O}_sotagrid.log 2>&1; tail -3 ${O}_sotagrid.log ;;
     single) timeout 600 python scripts/perf.py single --shapes C3,C1 > ${O}_single.log 2>&1; cat ${O}_single.log ;;
     perf) timeout 900 python scripts/perf.py time --shapes C1,C3,1x16k,C2,C4shard,C2fp8 > ${O}_perf.log 2>&1; cat ${O}_perf.log ;;
+    narrow) for c in '{"TILE_N": 16, "num_splits": 0, "num_stages": 4}' '{"TILE_N": 128, "num_splits": 0, "num_stages": 4}'; do
+              timeout 900 python scripts/perf.py time --shapes C2kv2,C2kv1,C4kv1,C4kv4,b4096 --cfg "$c" --tag narrow
+            done > ${O}_narrow.log 2>&1; cat ${O}_narrow.log ;;
+    e2e) timeout 600 python scripts/perf.py e2e > ${O}_e2e.log 2>&1; cat ${O}_e2e.log ;;
     *) echo "unknown recipe $r" >&2 ;;
   esac
 done

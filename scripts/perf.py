@@ -7,6 +7,7 @@
   perf.py prof    --op prefill|decode|c1 [--cfg json] [--n 3]   -- small driver for ncu / sanitizers
   perf.py trace   [BLOCK_M num_stages num_warps]                 -- clock64 trace (needs a -DB200_TRACE build)
   perf.py umma-rate                                              -- tcgen05 MMA issue-rate probe
+  perf.py e2e                                                    -- e2e decode step breakdown (C2)
 """
 
 from __future__ import annotations
@@ -33,6 +34,12 @@ SHAPES = {
     "4x8k": ("prefill", dict(W.C1, batch_size=4, seq_len=8192)),
     "C2": ("decode", W.C2), "C4shard": ("decode", dict(W.C4, batch_size=32)),
     "C2fp8": ("decode", dict(W.C2, kv_dtype="fp8_e4m3")), "b1x32k": ("decode", dict(W.C2, batch_size=1, seq_len=32768)),
+    # kv-head shards (one GPU's share when the kv heads are split): C2 over 4 / 8 GPUs, C4 over 8
+    "C2kv2": ("decode", dict(W.C2, num_q_heads=8, num_kv_heads=2)),
+    "C2kv1": ("decode", dict(W.C2, num_q_heads=4, num_kv_heads=1)),
+    "C4kv1": ("decode", dict(W.C4, num_q_heads=8, num_kv_heads=1)),
+    "C4kv4": ("decode", dict(W.C4, batch_size=64, num_q_heads=32, num_kv_heads=4)),
+    "b4096": ("decode", dict(W.C2, batch_size=4096, seq_len=256)),
 }
 
 
@@ -166,9 +173,53 @@ def cmd_umma_rate(a):
         print(f"{name:34s}: {cyc:7.1f} cycles / 8 MMAs (floor {ideal:.0f}) -> {ideal / cyc * 100:.0f}% of floor")
 
 
+def cmd_e2e(a):
+    """Where the e2e decode step's time goes (C2): device-only plan, the copies alone, append alone,
+    and attention.DecodeStep (one graph: H2D -> append -> decode -> D2H) at several chunk counts."""
+    d = W.make_decode(W.C2, device="cuda")
+    B, Hq, D = d.q.shape
+    Hkv, bs = d.k_cache.shape[2], d.k_cache.shape[1]
+    st = torch.cuda.current_stream()
+
+    def ev_time(fn, n=20):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        s.record(st)
+        for _ in range(n):
+            fn()
+        e.record(st)
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) * 1e3 / n, (time.perf_counter() - t0) * 1e6 / n
+
+    res = {}
+    plan = A.DecodePlan(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens, max_seq_len=d.max_seq_len)
+    res["decode_graph_us"] = graph_ms(plan.run, 20) * 1e3
+    nk = torch.randn(B, Hkv, D, device="cuda").bfloat16()
+    slots = torch.full((B,), -1, dtype=torch.int64, device="cuda")
+    res["append_graph_us"] = graph_ms(lambda: A.cache_append(nk, nk, d.k_cache, d.v_cache, slots), 20) * 1e3
+    for nbytes, name in ((787200, "h2d_787KB"), (524288, "d2h_512KB")):
+        h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        dd = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        f = (lambda: dd.copy_(h, non_blocking=True)) if name.startswith("h2d") else (lambda: h.copy_(dd, non_blocking=True))
+        res[name + "_us"] = ev_time(f)[0]
+    slots_h = torch.full((B,), -1, dtype=torch.int64)
+    for chunks in (1, 2, 3, 4, 8):
+        step = A.DecodeStep(d.k_cache, d.v_cache, d.block_table, batch=B, num_q_heads=Hq, max_seq_len=d.max_seq_len,
+                            chunks=chunks)
+        step.set_inputs(d.q.cpu(), nk.cpu(), nk.cpu(), slots_h, d.seq_lens.cpu())
+        dev_us, wall_us = ev_time(step)
+        res[f"step_chunks{chunks}_us"] = dev_us
+        res[f"step_chunks{chunks}_wall_us"] = wall_us
+        del step
+    print(json.dumps({"tag": a.tag, **{k: round(v, 2) for k, v in res.items()}}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("cmd", choices=["time", "single", "prof", "trace", "umma-rate"])
+    ap.add_argument("cmd", choices=["time", "single", "prof", "trace", "umma-rate", "e2e"])
     ap.add_argument("args", nargs="*")
     ap.add_argument("--op", default="prefill")
     ap.add_argument("--shapes", default="C3")
@@ -178,7 +229,7 @@ def main():
     ap.add_argument("--n", type=int, default=3)
     ap.add_argument("--tag", default="")
     a = ap.parse_args()
-    {"time": cmd_time, "single": cmd_single, "prof": cmd_prof, "trace": cmd_trace, "umma-rate": cmd_umma_rate}[a.cmd](a)
+    {"time": cmd_time, "single": cmd_single, "prof": cmd_prof, "trace": cmd_trace, "umma-rate": cmd_umma_rate, "e2e": cmd_e2e}[a.cmd](a)
 
 
 if __name__ == "__main__":

@@ -2,7 +2,7 @@
 # compute-sanitizer memcheck / racecheck / synccheck over small cases of every kernel (
 # VERDICT r1 "sanitizer pass"): K1 prefill (1 and 2 q heads per CTA, 4 and 8 softmax warps per
 # tile, causal + non-causal, varlen with the schedule kernel), K2' flat decode (bf16 + fp8 caches,
-# fused in-kernel merge and the K3' combine path), K2/K3 split decode, cache_append (+fp8).
+# fused in-kernel merge and the K3' combine path; Hkv = 1/2/4; batch > 1024), K2/K3 split decode, cache_append (+fp8).
 # Usage: bash scripts/sanitize.sh OUT_PREFIX   -> OUT_PREFIX_{memcheck,racecheck,synccheck}.log
 set -u
 OUT=${1:-gpurun_out/sanitize}
@@ -27,6 +27,12 @@ for B, cfg in ((64, dict(num_splits=0, num_stages=4, TILE_N=16)), (3, dict(num_s
     A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens, config=cfg)
     nk = torch.randn(B, 8, 128, device="cuda").bfloat16()
     A.cache_append(nk, nk, d.k_cache, d.v_cache, torch.arange(B, device="cuda") * 3)
+for hkv, bs in ((1, 16), (2, 32), (4, 16)):  # K2' at Hkv < 8 (PPT = 8 / Hkv page chunks per tile)
+    d = W.make_decode(dict(W.C2, batch_size=4, seq_len=300, num_q_heads=8 * hkv, num_kv_heads=hkv, block_size=bs),
+                      device="cuda", lens=[300, 1, 77, 129])
+    A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens, config=dict(num_splits=0, num_stages=4, TILE_N=16))
+d = W.make_decode(dict(W.C2, batch_size=1100, seq_len=40), device="cuda", lens=[40, 1, 17] * 366 + [5, 5])
+A.paged_decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens, config=dict(num_splits=0, num_stages=4, TILE_N=16))
 f = W.make_decode(dict(W.C2, batch_size=3, seq_len=300, kv_dtype="fp8_e4m3"), device="cuda", lens=[300, 5, 64])
 A.paged_decode(f.q, f.k_cache, f.v_cache, f.block_table, f.seq_lens, k_scale=f.k_scale, v_scale=f.v_scale)
 nk = torch.randn(3, 8, 128, device="cuda").bfloat16()

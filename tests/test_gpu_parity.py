@@ -323,6 +323,72 @@ def test_decode_flat_every_variant(hq, ns):
     check(f"decode flat hq={hq} stages={ns}", out, ref, base)
 
 
+# K2' at Hkv < 8: PPT = 8 / Hkv page chunks per 128-row tile (the kv-head shards of GQA models)
+NARROW = [(4, 4, 4), (4, 8, 4), (4, 16, 4), (4, 32, 4), (4, 8, 5), (4, 16, 5), (2, 2, 4), (2, 4, 4), (2, 8, 4),
+          (2, 16, 4), (2, 8, 5), (2, 16, 5), (1, 1, 4), (1, 2, 4), (1, 4, 4), (1, 8, 4), (1, 8, 5)]
+
+
+@pytest.mark.parametrize("hkv,hq,ns", NARROW, ids=lambda v: str(v))
+def test_decode_flat_narrow_kv_heads(hkv, hq, ns):
+    """every compiled Hkv = 1/2/4 flat variant; lengths that end mid-chunk, mid-tile and at 1."""
+    out, ref, base = run_decode([1000, 333, 17, 1, 129], Hq=hq, Hkv=hkv, cfg=dcfg(0, ns, 16))
+    check(f"decode flat hkv={hkv} hq={hq} stages={ns}", out, ref, base)
+
+
+@pytest.mark.parametrize("hkv", [1, 2, 4])
+@pytest.mark.parametrize("bs", [16, 32, 128])
+def test_decode_flat_narrow_block_sizes_and_nan_tails(hkv, bs):
+    """Hkv < 8 with pages of 16..128 tokens; slots past each sequence's end hold NaN (a tile's
+    chunks past the end reload a live chunk and are masked; the V rows are zeroed before PV)."""
+    lens = [33, 250, 16, 700]
+    shape = dict(W.C2, batch_size=4, seq_len=700, num_q_heads=8 * hkv, num_kv_heads=hkv, block_size=bs)
+    d = W.make_decode(shape, device="cpu", lens=lens, extra_blocks=2)
+    kc, vc = d.k_cache.clone(), d.v_cache.clone()
+    live = torch.zeros(kc.shape[0], bs, dtype=torch.bool)
+    for b, n in enumerate(lens):
+        for t in range(n):
+            live[d.block_table[b, t // bs], t % bs] = True
+    kc[~live] = float("nan")
+    vc[~live] = float("nan")
+    ref = oracle.decode(d.q, kc, vc, d.block_table, d.seq_lens)
+    args = [t.to(DEV) for t in (d.q, kc, vc, d.block_table, d.seq_lens)]
+    out = A.paged_decode(*args, config=dcfg(0, 4, 16))
+    assert not torch.isnan(out).any()
+    check(f"decode flat hkv={hkv} bs={bs} NaN tails", out, ref, sdpa_decode_bf16(*args))
+
+
+def test_decode_flat_kv_head_shard_of_c4():
+    """The C4 geometry sharded by kv head over 8 GPUs: each GPU holds Hkv = 1 with its 8 q heads
+    (64q/8kv -> 8q/1kv), ctx 32k — K2' at PPT = 8, every sequence vs the oracle."""
+    shape = dict(W.C4, batch_size=6, num_q_heads=8, num_kv_heads=1)
+    d = W.make_decode(shape, device="cpu", lens=[32768, 32768, 32767, 20000, 4096, 1])
+    ref = oracle.decode(d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)
+    args = [t.to(DEV) for t in (d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)]
+    plan = A.DecodePlan(*args)
+    assert plan.config["TILE_N"] == 16, plan.config  # the dispatcher picks the flat kernel for Hkv = 1
+    out = plan.run()
+    check("decode C4 kv-head shard (8q/1kv, 32k)", out, ref, sdpa_decode_bf16(*args))
+
+
+def test_decode_flat_batch_above_1024():
+    """3000 ragged sequences (batch > the 1024 fused-merge counters): the per-sequence tile prefix
+    is sized per launch and split sequences are merged by K3'."""
+    g = torch.Generator().manual_seed(5)
+    lens = torch.randint(1, 400, (3000,), generator=g).tolist()
+    lens[10] = 0
+    lens[2999] = 5000
+    shape = dict(W.C2, batch_size=len(lens), seq_len=max(lens))
+    d = W.make_decode(shape, device="cpu", lens=lens, extra_blocks=1)
+    args = [t.to(DEV) for t in (d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)]
+    out = A.paged_decode(*args, config=FLAT)
+    assert out[10].abs().max().item() == 0
+    sub = [0, 1, 500, 1023, 1024, 1025, 2000, 2998, 2999]
+    ref = oracle.decode(d.q[sub], d.k_cache, d.v_cache, d.block_table[sub], d.seq_lens[sub])
+    ki = torch.tensor(sub, device=DEV)
+    base = sdpa_decode_bf16(args[0][ki], args[1], args[2], args[3][ki], args[4][ki])
+    check("decode flat B=3000 ragged", out[sub], ref, base)
+
+
 def test_decode_flat_many_short_sequences():
     """300 ragged sequences: every CTA range spans many sequences and pieces of sequences."""
     g = torch.Generator().manual_seed(11)
@@ -504,8 +570,9 @@ def test_append_then_decode_equals_oracle():
 
 
 # ------------------------------------------------------------------ fp8 (e4m3) KV cache
-def run_decode_fp8(lens, Hq=32, cfg=None, seed=0, nan_tails=False):
-    shape = dict(W.C2, batch_size=len(lens), seq_len=max(lens), num_q_heads=Hq, seed=seed, kv_dtype="fp8_e4m3")
+def run_decode_fp8(lens, Hq=32, cfg=None, seed=0, nan_tails=False, Hkv=8):
+    shape = dict(W.C2, batch_size=len(lens), seq_len=max(lens), num_q_heads=Hq, num_kv_heads=Hkv, seed=seed,
+                 kv_dtype="fp8_e4m3")
     d = W.make_decode(shape, device="cpu", lens=lens, extra_blocks=3)
     kc, vc = d.k_cache.clone(), d.v_cache.clone()
     if nan_tails:  # e4m3 NaN codes (0x7f / 0xff) in every slot no sequence owns
@@ -530,6 +597,15 @@ def run_decode_fp8(lens, Hq=32, cfg=None, seed=0, nan_tails=False):
 def test_decode_fp8_every_variant(hq, ns):
     out, ref, base = run_decode_fp8([1000, 333, 17, 1], Hq=hq, cfg=dcfg(0, ns, 16))
     check(f"decode fp8 hq={hq} stages={ns}", out, ref, base)
+
+
+@pytest.mark.parametrize("hkv,hq,ns", [(4, 8, 8), (4, 16, 8), (4, 32, 6), (2, 8, 8), (2, 16, 6), (1, 8, 8)],
+                         ids=lambda v: str(v))
+def test_decode_fp8_narrow_kv_heads(hkv, hq, ns):
+    """fp8 K2' at Hkv < 8 (16-token chunks of Hkv heads per TMA box, PPT chunks per tile), NaN tails."""
+    out, ref, base = run_decode_fp8([1000, 333, 17, 1], Hq=hq, Hkv=hkv, cfg=dcfg(0, ns, 16), nan_tails=True)
+    assert not torch.isnan(out).any()
+    check(f"decode fp8 hkv={hkv} hq={hq} stages={ns}", out, ref, base)
 
 
 def test_decode_fp8_many_ragged_sequences_and_nan_tails():
