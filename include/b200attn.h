@@ -131,6 +131,8 @@ int b200attn_prefill(const b200attn_prefill_params* p, const b200attn_prefill_va
  * CTAs (batch >= ~num_SMs / 8), else by the K3' combine launch. */
 size_t b200attn_decode_workspace_size(const b200attn_decode_params* p, const b200attn_decode_variant* v);
 int b200attn_decode_num_splits(const b200attn_decode_params* p, const b200attn_decode_variant* v);
+/* Number of kernels b200attn_decode enqueues for this shape and config (1 or 2), or -1 if invalid. */
+int b200attn_decode_launches(const b200attn_decode_params* p, const b200attn_decode_variant* v);
 int b200attn_decode(const b200attn_decode_params* p, const b200attn_decode_variant* v, void* stream);
 /* K2 alone: with num_splits > 1 it leaves the unnormalised partials in the workspace (layout: a
  * 4096-byte counter header, then part_o [batch*Hq, splits, 128] fp32, then part_ml [batch*Hq, splits, 2])

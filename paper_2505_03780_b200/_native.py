@@ -71,7 +71,8 @@ STATUS_NAMES = {OK: "ok", UNSUPPORTED_CONFIG: "unsupported_config", SMEM_OVERFLO
 EXPORTS = (
     "b200attn_abi_version", "b200attn_build_info", "b200attn_status_string", "b200attn_last_error",
     "b200attn_prefill_supported", "b200attn_decode_supported", "b200attn_prefill_workspace_size", "b200attn_prefill",
-    "b200attn_decode_workspace_size", "b200attn_decode_num_splits", "b200attn_decode", "b200attn_decode_partial",
+    "b200attn_decode_workspace_size", "b200attn_decode_num_splits", "b200attn_decode_launches", "b200attn_decode",
+    "b200attn_decode_partial",
     "b200attn_combine",
     "b200attn_cache_append", "b200attn_cache_append_fp8", "b200attn_selftest_umma",
 )
@@ -105,6 +106,7 @@ def load():
     lib.b200attn_decode_workspace_size.argtypes = [DP, DV]
     lib.b200attn_decode_workspace_size.restype = ctypes.c_size_t
     lib.b200attn_decode_num_splits.argtypes = [DP, DV]
+    lib.b200attn_decode_launches.argtypes = [DP, DV]
     lib.b200attn_combine.argtypes = [_P, _P, _P, _I, _I, _P]
     lib.b200attn_cache_append.argtypes = [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P]
     lib.b200attn_cache_append_fp8.argtypes = [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, ctypes.c_float,
@@ -113,7 +115,7 @@ def load():
     for name in ("b200attn_prefill_supported", "b200attn_decode_supported", "b200attn_prefill", "b200attn_decode",
                  "b200attn_decode_partial",
                  "b200attn_combine", "b200attn_cache_append", "b200attn_cache_append_fp8", "b200attn_selftest_umma",
-                 "b200attn_decode_num_splits"):
+                 "b200attn_decode_num_splits", "b200attn_decode_launches"):
         getattr(lib, name).restype = ctypes.c_int
     if lib.b200attn_abi_version() != ABI_VERSION:
         raise RuntimeError(f"libb200attn ABI {lib.b200attn_abi_version()} != {ABI_VERSION}; rebuild the library")

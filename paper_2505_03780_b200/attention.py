@@ -197,6 +197,23 @@ def decode_supported(q_shape, cache_shape, max_blocks_per_seq, max_seq_len, conf
     return rc, buf.value.decode()
 
 
+def _decode_config(q, k_cache, block_table, max_seq_len) -> dict:
+    """The dispatch table's config for this shape; a flat (TILE_N = 16) pick whose smem does not fit
+    (very large batches keep a per-sequence prefix in smem) drops to the deepest ring that fits, else
+    to the split kernel."""
+    kv = _kv_name(k_cache)
+    cfg = default_decode_config(batch_size=q.shape[0], seq_len=int(max_seq_len), num_q_heads=q.shape[1],
+                                num_kv_heads=k_cache.shape[2], head_dim=q.shape[2], block_size=k_cache.shape[1],
+                                kv_dtype=kv)
+    if int(cfg["TILE_N"]) != 16 or q.shape[0] <= 1024:
+        return cfg
+    for ns in range(int(cfg["num_stages"]), 1, -1):
+        c = dict(cfg, num_stages=ns)
+        if decode_supported(tuple(q.shape), tuple(k_cache.shape), block_table.shape[1], int(max_seq_len), c, kv)[0] == 0:
+            return c
+    return dict(num_splits=0, num_stages=4, TILE_N=128)
+
+
 def paged_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, block_table: torch.Tensor,
                  seq_lens: torch.Tensor, max_seq_len: Optional[int] = None, out: Optional[torch.Tensor] = None,
                  softmax_scale: Optional[float] = None, config: Optional[Mapping] = None,
@@ -214,9 +231,7 @@ def paged_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, 
         if out is None:
             out = torch.empty_like(q)
         if config is None:
-            config = default_decode_config(batch_size=q.shape[0], seq_len=int(max_seq_len), num_q_heads=q.shape[1],
-                                           num_kv_heads=k_cache.shape[2], head_dim=q.shape[2],
-                                           block_size=k_cache.shape[1], kv_dtype=_kv_name(k_cache))
+            config = _decode_config(q, k_cache, block_table, max_seq_len)
         var = decode_variant(config)
         p = _decode_params(q, k_cache, v_cache, block_table, seq_lens, out, max_seq_len, softmax_scale,
                            k_scale=k_scale, v_scale=v_scale)
@@ -354,9 +369,7 @@ class DecodePlan:
         _check_decode_shapes(q, k_cache, v_cache, block_table, seq_lens, out)
         self.max_seq_len = int(max_seq_len if max_seq_len is not None else block_table.shape[1] * k_cache.shape[1])
         self.out = torch.empty_like(q) if out is None else out
-        self.config = dict(config or default_decode_config(
-            batch_size=q.shape[0], seq_len=self.max_seq_len, num_q_heads=q.shape[1], num_kv_heads=k_cache.shape[2],
-            head_dim=q.shape[2], block_size=k_cache.shape[1], kv_dtype=_kv_name(k_cache)))
+        self.config = dict(config or _decode_config(q, k_cache, block_table, self.max_seq_len))
         self.var = decode_variant(self.config)
         self.p = _decode_params(q, k_cache, v_cache, block_table, seq_lens, self.out, self.max_seq_len, softmax_scale,
                                 k_scale=k_scale, v_scale=v_scale)
@@ -371,7 +384,7 @@ class DecodePlan:
         self._tensors = (q, k_cache, v_cache, block_table, seq_lens, self.out)
 
     def kernels_per_run(self) -> int:
-        return 2 if (self.num_splits > 1 or int(self.config["TILE_N"]) == 16) else 1
+        return int(self.lib.b200attn_decode_launches(self.p, self.var))
 
     def run(self, stream=None):
         with _on(self.device):

@@ -63,6 +63,35 @@ void copy_reason(char* dst, size_t n) {
   }
 }
 
+// ------------------------------------------------------------------ launches
+// Programmatic dependent launch (sm_90+): the kernel's prologue overlaps the previous kernel's tail
+// in the stream (the kernels call griddep_wait() before touching global memory).  On by default;
+// B200ATTN_PDL=0 launches plainly (A/B).
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("B200ATTN_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ------------------------------------------------------------------ tensor maps
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -128,8 +157,16 @@ int ensure_smem_attr(const void* kern, int bytes, const char* what) {
     std::lock_guard<std::mutex> g(mu);
     if (done.count({kern, dev})) return B200ATTN_OK;
   }
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, kern);
   if (e != cudaSuccess) return cuda_fail(e, what);
+  // the opt-in limit covers static + dynamic shared memory
+  if (bytes + (int)fa.sharedSizeBytes > kMaxSmem) bytes = kMaxSmem - (int)fa.sharedSizeBytes;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // not sticky: keep it from surfacing in the next launch's error check
+    return cuda_fail(e, what);
+  }
   std::lock_guard<std::mutex> g(mu);
   done.insert({kern, dev});
   return B200ATTN_OK;
@@ -190,12 +227,11 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   if (!single) {
     const size_t hist_bytes = (size_t)nkeys * sizeof(int32_t);
     if (hist_bytes <= 40 * 1024)
-      b200::prefill_schedule_kernel<true><<<1, 1024, hist_bytes, stream>>>(p->cu_seqlens, p->num_seqs, p->causal,
-                                                                           nkeys, ws);
+      e = launch_k(b200::prefill_schedule_kernel<true>, dim3(1), dim3(1024), hist_bytes, stream, p->cu_seqlens,
+                   p->num_seqs, p->causal, nkeys, ws);
     else
-      b200::prefill_schedule_kernel<false><<<1, 1024, 0, stream>>>(p->cu_seqlens, p->num_seqs, p->causal, nkeys,
-                                                                   ws);
-    e = cudaGetLastError();
+      e = launch_k(b200::prefill_schedule_kernel<false>, dim3(1), dim3(1024), 0, stream, p->cu_seqlens, p->num_seqs,
+                   p->causal, nkeys, ws);
     if (e != cudaSuccess) return cuda_fail(e, "prefill schedule launch");
   }
   b200::PrefillKernelArgs a;
@@ -216,8 +252,7 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   // persistent: never more CTAs than work items (upper bound without a device read)
   const long long items_ub = ((long long)p->total_tokens / 128 + p->num_seqs) * a.num_hg;
   const int ctas = (int)std::min<long long>(num_sms(), std::max<long long>(1, items_ub));
-  kern<<<ctas, C::NTHREADS, C::SMEM_BYTES, stream>>>(mq, mk, mv, a);
-  e = cudaGetLastError();
+  e = launch_k(kern, dim3(ctas), dim3(C::NTHREADS), C::SMEM_BYTES, stream, mq, mk, mv, a);
   if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
   return B200ATTN_OK;
 }
@@ -400,7 +435,7 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
   auto kern = b200::decode_flat_kernel<HKV, G, NS, FP8>;
   // the per-sequence tile prefix lives in smem: the launch's dynamic size grows with the batch
   const int smem = C::smem_bytes(p->batch);
-  if (smem > kMaxSmem)
+  if (smem + 64 > kMaxSmem)  // + the kernel's static shared memory (the scan's warp totals)
     return fail(B200ATTN_SMEM_OVERFLOW, "decode_flat: batch %d needs %d B smem > %d", p->batch, smem, kMaxSmem);
   if (int rc0 = ensure_smem_attr(reinterpret_cast<const void*>(kern), kMaxSmem, "cudaFuncSetAttribute(decode_flat)"))
     return rc0;
@@ -445,13 +480,12 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
     a.scale_log2 *= (p->k_scale > 0.f ? p->k_scale : 1.f);
     a.out_scale = (p->v_scale > 0.f ? p->v_scale : 1.f);
   }
-  kern<<<ctas, C::NTHREADS, smem, stream>>>(mq, mk, mv, a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(kern, dim3(ctas), dim3(C::NTHREADS), smem, stream, mq, mk, mv, a);
   if (e != cudaSuccess) return cuda_fail(e, "decode_flat launch");
   if (combine && !fused) {
-    b200::flat_combine_kernel<C::NQ><<<dim3(p->batch, C::NQ), 128, 0, stream>>>(
-        a.part_o, a.part_ml, a.cu_tiles_out, p->batch, ctas, reinterpret_cast<__nv_bfloat16*>(p->o));
-    e = cudaGetLastError();
+    e = launch_k(b200::flat_combine_kernel<C::NQ>, dim3(p->batch, C::NQ), dim3(128), 0, stream,
+                 (const float*)a.part_o, (const float*)a.part_ml, (const int32_t*)a.cu_tiles_out, (int)p->batch, ctas,
+                 reinterpret_cast<__nv_bfloat16*>(p->o));
     if (e != cudaSuccess) return cuda_fail(e, "flat combine launch");
   }
   return B200ATTN_OK;
@@ -510,7 +544,7 @@ int check_flat(const b200attn_decode_params* p, const b200attn_decode_variant* v
                 v->num_stages, H, G);
   }
   const int smem = e->smem + (p->batch - 1024) * 4;  // the cu array is sized per batch
-  if (smem > kMaxSmem)
+  if (smem + 64 > kMaxSmem)
     return fail(B200ATTN_SMEM_OVERFLOW, "decode_flat: batch %d needs %d B smem > %d", p->batch, smem, kMaxSmem);
   *out = e;
   return B200ATTN_OK;
@@ -672,6 +706,21 @@ int b200attn_decode_num_splits(const b200attn_decode_params* p, const b200attn_d
   int s, t;
   resolve_splits(p, v, c.split->smem, &s, &t);
   return s;
+}
+
+int b200attn_decode_launches(const b200attn_decode_params* p, const b200attn_decode_variant* v) {
+  DecodeChoice c;
+  if (resolve_decode(p, v, &c)) return -1;
+  if (c.flat) {  // K3' only when split sequences are not merged inside K2' (same rule as launch_flat)
+    const int tt = 128 / p->num_kv_heads;  // tokens per tile
+    const long long tiles_ub = (long long)p->batch * ((p->max_seq_len + tt - 1) / tt);
+    const int ctas = (int)std::max<long long>(1, std::min<long long>(num_sms(), (tiles_ub + kFlatMinTiles - 1) /
+                                                                                   kFlatMinTiles));
+    return flat_fused_merge(p->batch, ctas) ? 1 : 2;
+  }
+  int s, t;
+  resolve_splits(p, v, c.split->smem, &s, &t);
+  return s > 1 ? 2 : 1;
 }
 
 size_t b200attn_decode_workspace_size(const b200attn_decode_params* p, const b200attn_decode_variant* v) {

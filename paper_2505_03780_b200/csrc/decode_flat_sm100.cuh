@@ -238,6 +238,32 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
   const int warp = warp_id(), lane = lane_id();
   const int B = args.batch;
 
+  // zero Q (padded rows), the fp8 Q split and P^T (block-diagonal zeros) once
+  for (int i = threadIdx.x; i < (C::OFF_ALPHA - C::OFF_Q) / 16; i += C::NTHREADS)
+    reinterpret_cast<uint4*>(sQ)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 32) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&q_conv[i], 128);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 128);
+    }
+    for (int i = 0; i < NSTAGE; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == C::TMA_WARP && lane == 0) {
+    tma_prefetch_desc(&tmap_q);
+    tma_prefetch_desc(&tmap_k);
+    tma_prefetch_desc(&tmap_v);
+  }
+  griddep_wait();  // PDL: the prologue above overlapped the previous kernel; data access starts here
+  griddep_launch();
   // ---- tiles per sequence -> cu (exclusive prefix), block-wide: each thread scans a contiguous
   // chunk of sequences (any batch size, no serial chain of loads)
   {
@@ -261,25 +287,6 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
       run += (args.seq_lens[b] + C::TT - 1) / C::TT;
       cu[b + 1] = run;
     }
-  }
-  // zero Q (padded rows), the fp8 Q split and P^T (block-diagonal zeros) once
-  for (int i = threadIdx.x; i < (C::OFF_ALPHA - C::OFF_Q) / 16; i += C::NTHREADS)
-    reinterpret_cast<uint4*>(sQ)[i] = make_uint4(0, 0, 0, 0);
-  if (threadIdx.x == 32) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1);
-      mbar_init(&q_conv[i], 128);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
-      mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 128);
-    }
-    for (int i = 0; i < NSTAGE; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-    }
-    fence_barrier_init();
   }
   fence_proxy_async_smem();
   __syncthreads();
@@ -315,11 +322,6 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
 
   if (warp == C::TMA_WARP) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      tma_prefetch_desc(&tmap_q);
-      tma_prefetch_desc(&tmap_k);
-      tma_prefetch_desc(&tmap_v);
-    }
     const uint64_t stream_once = policy_evict_first();
     const int bs = args.block_size;
     int it = 0, k = 0, b = b_first;
@@ -741,6 +743,8 @@ __global__ void __launch_bounds__(128) flat_combine_kernel(const float* __restri
   __shared__ float red[4];
   __shared__ float4 acc_s[4][32];
   const int b = blockIdx.x, q = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  griddep_wait();  // PDL: K2' (the predecessor) has completed and its partials are visible
+  griddep_launch();
   const int ts = cu[b], te = cu[b + 1], n = cu[batch];
   __nv_bfloat16* out = o + (static_cast<size_t>(b) * NQ + q) * 128;
   if (ts == te) {

@@ -367,10 +367,17 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
     fence_barrier_init();
   }
   if (warp == C::MMA_WARP) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == C::TMA_WARP && lane == 0) {
+    tma_prefetch_desc(&tmap_q);
+    tma_prefetch_desc(&tmap_k);
+    tma_prefetch_desc(&tmap_v);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();    // PDL: the prologue above overlapped the previous kernel; data access starts here
+  griddep_launch();
   // register hand-over (REG_SPLIT): each role adjusts its own limit at the top of its branch, so
   // the allocator never sees a join of the two limits
   auto regs_other = [] {
@@ -386,9 +393,6 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
     // ------------------------------------------------------------ scheduler + TMA producer
     regs_other();
     if (lane == 0) {
-      tma_prefetch_desc(&tmap_q);
-      tma_prefetch_desc(&tmap_k);
-      tma_prefetch_desc(&tmap_v);
       const int total_work = (args.single_nqb > 0 ? args.single_nqb : args.sched[1]) * args.num_hg;
       const uint64_t keep = policy_evict_last();  // K/V tiles are re-read by other q blocks / heads
       int ri = 0;
@@ -686,6 +690,8 @@ __global__ void __launch_bounds__(1024) prefill_schedule_kernel(const int32_t* _
   int32_t* items = ws + 3 + nkeys;
   __shared__ int32_t part[1024];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  griddep_wait();  // PDL: the previous launch may still be reading this workspace
+  griddep_launch();
   for (int k = tid; k < nkeys; k += 1024) hist[k] = 0;
   __syncthreads();
   for (int s = warp; s < num_seqs; s += 32) {

@@ -38,6 +38,16 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// A kernel launched with the programmatic-serialization attribute may start while its predecessor
+// in the stream drains: everything before griddep_wait() (barrier init, TMEM alloc, descriptor
+// prefetch) overlaps the predecessor's tail; griddep_wait() returns once the predecessor grid has
+// completed and its memory is visible, so no global memory is touched before it.  Without the
+// attribute both are no-ops.  griddep_launch() lets the NEXT kernel in the stream start its own
+// prologue as soon as SMs free up (it still waits for this grid to finish before any data access).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

@@ -40,6 +40,10 @@ SHAPES = {
     "C4kv1": ("decode", dict(W.C4, num_q_heads=8, num_kv_heads=1)),
     "C4kv4": ("decode", dict(W.C4, batch_size=64, num_q_heads=32, num_kv_heads=4)),
     "b4096": ("decode", dict(W.C2, batch_size=4096, seq_len=256)),
+    # small, latency-bound decode shapes of the C5 grid
+    "d1x8k": ("decode", dict(W.C2, batch_size=1, seq_len=8192)), "d16x512": ("decode", dict(W.C2, batch_size=16, seq_len=512)),
+    "d4x2k": ("decode", dict(W.C2, batch_size=4, seq_len=2048)), "d1x512": ("decode", dict(W.C2, batch_size=1, seq_len=512)),
+    "d64x512": ("decode", dict(W.C2, batch_size=64, seq_len=512)),
 }
 
 

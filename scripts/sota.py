@@ -88,8 +88,9 @@ def prefill_cases(x, scale):
     B = len(lens)
     maxL = max(lens)
 
-    # flashinfer trtllm-gen context kernel (paged K/V, NHD)
-    def fi_trtllm():
+    # flashinfer trtllm-gen context kernel (paged K/V, NHD); PDL is the library's default on sm_100
+    # (programmatic dependent launch, which ours uses too) — timed with and without it
+    def fi_trtllm(pdl=True):
         import flashinfer
 
         bs = 32
@@ -101,10 +102,12 @@ def prefill_cases(x, scale):
 
         def f():
             return flashinfer.prefill.trtllm_batch_context_with_kv_cache(
-                q, (kc, vc), ws, bt, sl, maxL, maxL, scale, 1.0, B, cu, cu, out=out, kv_layout="NHD", causal=True)
+                q, (kc, vc), ws, bt, sl, maxL, maxL, scale, 1.0, B, cu, cu, out=out, kv_layout="NHD", causal=True,
+                enable_pdl=pdl)
         return f
 
     yield "flashinfer-trtllm-gen (fmhaSm100a)", fi_trtllm
+    yield "flashinfer-trtllm-gen (fmhaSm100a, no PDL)", lambda: fi_trtllm(False)
 
     def cudnn_sdpa():
         from torch.nn.attention import SDPBackend, sdpa_kernel
@@ -163,7 +166,7 @@ def decode_cases(d, scale):
     NB, bs, Hkv, _ = kc.shape
     maxL = d.max_seq_len
 
-    def fi_trtllm():
+    def fi_trtllm(pdl=True):
         import flashinfer
 
         ws = torch.zeros(256 << 20, dtype=torch.uint8, device=q.device)
@@ -171,10 +174,12 @@ def decode_cases(d, scale):
 
         def f():
             return flashinfer.decode.trtllm_batch_decode_with_kv_cache(
-                q, (kc, vc), ws, bt, sl, maxL, bmm1_scale=scale, bmm2_scale=1.0, out=out, kv_layout="NHD")
+                q, (kc, vc), ws, bt, sl, maxL, bmm1_scale=scale, bmm2_scale=1.0, out=out, kv_layout="NHD",
+                enable_pdl=pdl)
         return f
 
     yield "flashinfer-trtllm-gen decode (fmhaSm100a)", fi_trtllm
+    yield "flashinfer-trtllm-gen decode (fmhaSm100a, no PDL)", lambda: fi_trtllm(False)
 
     def fi_fa2():
         import flashinfer
@@ -305,16 +310,20 @@ def main():
     lines = []
     if args.grid:
         global prefill_cases, decode_cases
-        keep_pf = ("flashinfer-trtllm-gen (fmhaSm100a)", "cudnn-sdpa (torch, per sequence)")
-        keep_dec = ("flashinfer-trtllm-gen decode (fmhaSm100a)",)
+        keep_pf = ("flashinfer-trtllm-gen (fmhaSm100a)", "cudnn-sdpa (torch, per sequence)",
+                   "flashinfer-trtllm-gen (fmhaSm100a, no PDL)")
+        keep_dec = ("flashinfer-trtllm-gen decode (fmhaSm100a)", "flashinfer-trtllm-gen decode (fmhaSm100a, no PDL)")
         pf_all, dec_all = prefill_cases, decode_cases
         prefill_cases = lambda x, sc: ((n, f) for n, f in pf_all(x, sc) if n in keep_pf)  # noqa: E731
         decode_cases = lambda d, sc: ((n, f) for n, f in dec_all(d, sc) if n in keep_dec)  # noqa: E731
         for kind in ("prefill", "decode"):
             for name, shape in grid_shapes(kind):
                 run(name, kind, shape, lines, args.n)
-        summary = {"prefill": cdf([ln for ln in lines if ln["config"].startswith("prefill")], keep_pf),
-                   "decode": cdf([ln for ln in lines if ln["config"].startswith("decode")], keep_dec)}
+        pf = [ln for ln in lines if ln["config"].startswith("prefill")]
+        dec = [ln for ln in lines if ln["config"].startswith("decode")]
+        summary = {"prefill": cdf(pf, keep_pf[:2]), "decode": cdf(dec, keep_dec[:1]),
+                   "prefill_vs_pdl_off_libraries": cdf(pf, keep_pf[1:]),
+                   "decode_vs_pdl_off_library": cdf(dec, keep_dec[1:])}
         print(json.dumps({"relative_cdf_vs_best_library": summary}), flush=True)
         lines.append({"relative_cdf_vs_best_library": summary})
     else:

@@ -38,7 +38,7 @@ def test_kv_dtype_is_part_of_the_geometry(table):
     bf16 = D.default_decode_config(batch_size=64, seq_len=4096, block_size=16, **HEADS)
     assert bf16 == {"num_splits": 0, "num_stages": 5, "TILE_N": 16}
     fp8 = D.default_decode_config(batch_size=64, seq_len=4096, block_size=16, kv_dtype="fp8_e4m3", **HEADS)
-    assert fp8["TILE_N"] == 16 and fp8["num_stages"] == D.FP8_DECODE_STAGES[4]
+    assert fp8["TILE_N"] == 16 and fp8["num_stages"] == D.FP8_DECODE_STAGES[(8, 4)]
 
 
 def test_lookup_is_memoised_and_returns_copies(table):
@@ -73,3 +73,19 @@ def test_lookup_memo_is_bucketed_and_bounded(table, monkeypatch):
     for b in range(1, 200):
         D.default_decode_config(batch_size=b * 7, seq_len=4096, block_size=16, **HEADS)
     assert len(D._lookup_cache) <= 8
+
+
+def test_flat_kernel_covers_kv_head_shards_and_large_batches(table):
+    """K2' is compiled for 1/2/4/8 kv heads and any batch up to FLAT_MAX_BATCH; Hkv < 8 gets the ring
+    depth compiled for every GQA group; odd geometries still fall to the split kernel."""
+    assert D.flat_decode_ok(num_q_heads=8, num_kv_heads=1, block_size=16, batch_size=256)
+    assert D.flat_decode_ok(num_q_heads=8, num_kv_heads=2, block_size=32, batch_size=4096)
+    assert not D.flat_decode_ok(num_q_heads=12, num_kv_heads=3, block_size=16)
+    assert not D.flat_decode_ok(num_q_heads=8, num_kv_heads=8, block_size=48)
+    assert not D.flat_decode_ok(batch_size=D.FLAT_MAX_BATCH + 1)
+    c = D.default_decode_config(batch_size=256, seq_len=32768, num_q_heads=8, num_kv_heads=1, head_dim=128,
+                                block_size=16)
+    assert c == {"num_splits": 0, "num_stages": D.FLAT_STAGES_NARROW, "TILE_N": 16}
+    f = D.default_decode_config(batch_size=256, seq_len=32768, num_q_heads=8, num_kv_heads=1, head_dim=128,
+                                block_size=16, kv_dtype="fp8_e4m3")
+    assert f["TILE_N"] == 16 and f["num_stages"] == D.FP8_DECODE_STAGES[(1, 8)]
