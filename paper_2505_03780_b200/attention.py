@@ -468,7 +468,9 @@ class DecodeStep:
         Hkv, D = k_cache.shape[2], k_cache.shape[3]
         B, Hq = int(batch), int(num_q_heads)
         if chunks <= 0:
-            chunks = 2 if B >= 32 else 1
+            # one chunk: a decode launch per chunk costs more (ramp + tail) than the copies it hides
+            # (C2: 217 us at 1 chunk vs 233 / 262 / 239 us at 2 / 3 / 4, r2d perf.py e2e)
+            chunks = 1
         chunks = max(1, min(chunks, B))
         bounds = [B * i // chunks for i in range(chunks + 1)]
         self.bounds = bounds
@@ -504,6 +506,14 @@ class DecodeStep:
 
         def body():
             main = torch.cuda.current_stream(dev)
+            if chunks == 1:  # one stream: H2D -> append -> decode -> D2H, no cross-stream edges
+                lo, hi = ranges[0]
+                plan, dv = self.plans[0]
+                self.stage_d[lo:hi].copy_(self.stage_h[lo:hi], non_blocking=True)
+                cache_append(dv[1], dv[2], k_cache, v_cache, dv[3], k_scale=k_scale, v_scale=v_scale)
+                plan.run()
+                self.out_host.copy_(self.out_d, non_blocking=True)
+                return
             ev_in = [torch.cuda.Event() for _ in range(chunks)]
             ev_dec = [torch.cuda.Event() for _ in range(chunks)]
             self._cin.wait_stream(main)

@@ -30,11 +30,14 @@ def needs_build() -> bool:
     return any(s.stat().st_mtime > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Path:
+    """trace: a separate debug library (-DB200_TRACE: clock/globaltimer timelines) at
+    _lib/libb200attn_trace.so, loaded with B200ATTN_LIB=... by scripts/perf.py."""
+    out = OUT.with_name("libb200attn_trace.so") if trace else OUT
+    if not force and not trace and not needs_build():
         return OUT
     OUT.parent.mkdir(parents=True, exist_ok=True)
-    cmd = [NVCC, *FLAGS, "-o", str(OUT) + ".tmp", str(CSRC / "capi.cu")]
+    cmd = [NVCC, *FLAGS, *(["-DB200_TRACE"] if trace else []), "-o", str(out) + ".tmp", str(CSRC / "capi.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -43,9 +46,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError(f"nvcc failed ({r.returncode})")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(str(OUT) + ".tmp", OUT)
-    return OUT
+    os.replace(str(out) + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

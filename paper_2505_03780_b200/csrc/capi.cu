@@ -402,7 +402,25 @@ int num_sms() {  // per device (cached; a process may drive several GPUs)
   return n;
 }
 
-constexpr int kFlatMinTiles = 2;
+// Persistent CTAs, but at least flat_min_tiles() tiles each when the (host-known upper bound of the)
+// tile count is small: fewer partial segments to merge, same memory parallelism.
+// B200ATTN_FLAT_MIN_TILES overrides the default 2 (A/B).
+int flat_min_tiles() {
+  static int v = 0;
+  if (v == 0) {
+    const char* e = getenv("B200ATTN_FLAT_MIN_TILES");
+    v = (e && atoi(e) > 0) ? atoi(e) : 2;
+  }
+  return v;
+}
+
+// CTAs of a flat launch (launch_flat and b200attn_decode_launches agree on it)
+int flat_ctas(const b200attn_decode_params* p) {
+  const int tt = 128 / p->num_kv_heads;  // tokens per tile
+  const long long tiles_ub = (long long)p->batch * ((p->max_seq_len + tt - 1) / tt);
+  const int mt = flat_min_tiles();
+  return (int)std::max<long long>(1, std::min<long long>(num_sms(), (tiles_ub + mt - 1) / mt));
+}
 
 // Flat workspace: per-sequence arrival counters at a FIXED offset (see kFlatCounters), then
 // partials, then cu_tiles.
@@ -454,11 +472,7 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
     if ((rc = make_map_3d(&mk, p->k_cache, D, tokens, HKV, (uint64_t)HKV * D * 2, D * 2ull, 16, HKV))) return rc;
     if ((rc = make_map_3d(&mv, p->v_cache, D, tokens, HKV, (uint64_t)HKV * D * 2, D * 2ull, 16, HKV))) return rc;
   }
-  // persistent CTAs, but at least kFlatMinTiles tiles each when the (host-known upper bound of
-  // the) tile count is small: fewer partial segments to merge, same memory parallelism
-  const long long tiles_ub = (long long)p->batch * ((p->max_seq_len + C::TT - 1) / C::TT);
-  const int ctas = (int)std::max<long long>(1, std::min<long long>(num_sms(), (tiles_ub + kFlatMinTiles - 1) /
-                                                                                  kFlatMinTiles));
+  const int ctas = flat_ctas(p);
   const size_t slots = (size_t)num_sms() + p->batch;
   b200::FlatDecodeArgs a;
   a.block_table = p->block_table;
@@ -483,9 +497,11 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
   cudaError_t e = launch_k(kern, dim3(ctas), dim3(C::NTHREADS), smem, stream, mq, mk, mv, a);
   if (e != cudaSuccess) return cuda_fail(e, "decode_flat launch");
   if (combine && !fused) {
-    e = launch_k(b200::flat_combine_kernel<C::NQ>, dim3(p->batch, C::NQ), dim3(128), 0, stream,
-                 (const float*)a.part_o, (const float*)a.part_ml, (const int32_t*)a.cu_tiles_out, (int)p->batch, ctas,
-                 reinterpret_cast<__nv_bfloat16*>(p->o));
+    // a plain launch: with PDL its CTAs became resident beside K2' and the 1-sequence x 8k decode lost
+    // 6 us (22.1 vs 15.9 us, r2d pdlab); K2' of the next step still overlaps this kernel's tail
+    b200::flat_combine_kernel<C::NQ><<<dim3(p->batch, C::NQ), 128, 0, stream>>>(
+        a.part_o, a.part_ml, a.cu_tiles_out, p->batch, ctas, reinterpret_cast<__nv_bfloat16*>(p->o));
+    e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "flat combine launch");
   }
   return B200ATTN_OK;
@@ -712,11 +728,7 @@ int b200attn_decode_launches(const b200attn_decode_params* p, const b200attn_dec
   DecodeChoice c;
   if (resolve_decode(p, v, &c)) return -1;
   if (c.flat) {  // K3' only when split sequences are not merged inside K2' (same rule as launch_flat)
-    const int tt = 128 / p->num_kv_heads;  // tokens per tile
-    const long long tiles_ub = (long long)p->batch * ((p->max_seq_len + tt - 1) / tt);
-    const int ctas = (int)std::max<long long>(1, std::min<long long>(num_sms(), (tiles_ub + kFlatMinTiles - 1) /
-                                                                                   kFlatMinTiles));
-    return flat_fused_merge(p->batch, ctas) ? 1 : 2;
+    return flat_fused_merge(p->batch, flat_ctas(p)) ? 1 : 2;
   }
   int s, t;
   resolve_splits(p, v, c.split->smem, &s, &t);
@@ -822,6 +834,9 @@ int b200attn_cache_append_fp8(const void* new_k, const void* new_v, void* k_cach
 #ifdef B200_TRACE
 int b200attn_debug_trace(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, b200::g_trace, sizeof(unsigned long long) * (size_t)n);
+}
+int b200attn_debug_dtrace(unsigned long long* host, int n) {  // K2' per-CTA timeline [1024][8]
+  return (int)cudaMemcpyFromSymbol(host, b200::g_dtrace, sizeof(unsigned long long) * (size_t)n);
 }
 #endif
 

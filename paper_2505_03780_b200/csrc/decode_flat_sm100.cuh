@@ -88,6 +88,25 @@ struct FlatCfg {
   static constexpr int WCOLS = HKV >= 2 ? 2 * G : G;
 };
 
+#ifdef B200_TRACE
+// debug-only per-CTA timeline (%globaltimer ns): 0 entry, 1 after the tile scan, 2 first S seen by the
+// softmax, 3 last P of the range, 4 last segment's output / partial written, 5 merge done, 6 exit
+__device__ unsigned long long g_dtrace[1024][8];
+__device__ __forceinline__ void dtrace(int ev) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (blockIdx.x < 1024) g_dtrace[blockIdx.x][ev] = t;
+}
+#define DTRACE(ev, cond) \
+  do {                   \
+    if (cond) dtrace(ev); \
+  } while (0)
+#else
+#define DTRACE(ev, cond) \
+  do {                   \
+  } while (0)
+#endif
+
 __device__ __forceinline__ int flat_cta_of(int t, int ctas, int ntiles) {
   return static_cast<int>(((static_cast<long long>(t) + 1) * ctas - 1) / ntiles);
 }
@@ -237,6 +256,7 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS);
   const int warp = warp_id(), lane = lane_id();
   const int B = args.batch;
+  DTRACE(0, threadIdx.x == 0);
 
   // zero Q (padded rows), the fp8 Q split and P^T (block-diagonal zeros) once
   for (int i = threadIdx.x; i < (C::OFF_ALPHA - C::OFF_Q) / 16; i += C::NTHREADS)
@@ -290,6 +310,7 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
   }
   fence_proxy_async_smem();
   __syncthreads();
+  DTRACE(1, threadIdx.x == 0);
   const int ntiles = cu[B];
   const int T0 = static_cast<int>(static_cast<long long>(blockIdx.x) * ntiles / gridDim.x);
   const int T1 = static_cast<int>((static_cast<long long>(blockIdx.x) + 1) * ntiles / gridDim.x);
@@ -345,6 +366,11 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
         const int n = min(TPB, seg_end - base);
         int page = 0;
         if (lane < n * PPT) page = __ldg(bt + chunk_tok((base - tile0) * PPT + lane) / bs);
+        // lane l holds the page of chunk l of this batch and issues its boxes itself: PPT lanes
+        // issue a tile's PPT chunks at once (at Hkv = 1 a tile is 8 pages x 2 boxes per operand —
+        // one issuing thread was the bottleneck)
+        const int my_tok = chunk_tok((base - tile0) * PPT + lane);
+        const int my_row = page * bs + (my_tok & (bs - 1));
         for (int j = 0; j < n; ++j) {
 #pragma unroll
           for (int kv = 0; kv < 2; ++kv, ++it) {
@@ -355,16 +381,12 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
               mbar_wait(&kv_empty[slot], ((it / NSTAGE) & 1) ^ 1);
               mbar_arrive_expect_tx(&kv_full[slot], C::SLOT);
             }
-#pragma unroll
-            for (int pc = 0; pc < PPT; ++pc) {
-              const int pg = __shfl_sync(0xffffffffu, page, j * PPT + pc);
-              const int tok = chunk_tok((base + j - tile0) * PPT + pc);
-              const int row = pg * bs + (tok & (bs - 1));
-              if (lane == 0) {
-                uint8_t* d = dst + pc * 16 * HKV * 128;  // rows (chunk, head, token) of 128 B per half
-                tma_load_3d_hint(d, map, &kv_full[slot], 0, row, 0, stream_once);
-                if (!FP8) tma_load_3d_hint(d + C::HALF, map, &kv_full[slot], 64, row, 0, stream_once);
-              }
+            __syncwarp();  // the slot is free before any lane's TMA writes into it
+            const int pc = lane - j * PPT;
+            if (pc >= 0 && pc < PPT) {
+              uint8_t* d = dst + pc * 16 * HKV * 128;  // rows (chunk, head, token) of 128 B per half
+              tma_load_3d_hint(d, map, &kv_full[slot], 0, my_row, 0, stream_once);
+              if (!FP8) tma_load_3d_hint(d + C::HALF, map, &kv_full[slot], 64, my_row, 0, stream_once);
             }
           }
         }
@@ -523,6 +545,7 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
         // QK(i) and tcgen05 ops complete in order, so this wait returns at once
         if (i >= 2) mbar_wait(&o_full[(i - 2) & 1], ((i - 2) >> 1) & 1);
         tc_fence_after();
+        DTRACE(2, row == 0 && i == 0);
         const int tok = (t - tile0) * C::TT + pch * 16 + t16;
         const bool valid = tok < len;
         float x[G];
@@ -649,6 +672,7 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
+        DTRACE(3, row == 0 && t == T1 - 1);
       }
 
       // ---- segment epilogue: O^T (TMEM) / l, or the unnormalised partial for K3'
@@ -712,8 +736,10 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
           args.part_ml[(slot * NQ + row) * 2 + 0] = ml_s[row];
           args.part_ml[(slot * NQ + row) * 2 + 1] = ml_s[NP + row];
         }
+        DTRACE(4, row == 0 && seg_end == T1);
         if (args.seq_cnt != nullptr) flat_merge_if_last<NQ, NP>(args, r, ml_s, flags, cu, b, ntiles, row);
       }
+      DTRACE(5, row == 0 && seg_end == T1);
       named_bar_sync(1, 128);  // ml_s reads done before the next segment's epilogue rewrites it
     }
   }
@@ -725,6 +751,7 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
   }
+  DTRACE(6, threadIdx.x == 0);
 }
 
 // K3': merge the partial segments of every split sequence (sequences finished inside one CTA

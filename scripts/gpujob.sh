@@ -13,7 +13,7 @@
 #   sota       scripts/sota.py (same-box library comparators)   single    single-launch vs amortised
 #   sotagrid   scripts/sota.py --grid (C5 grid, relative_cdf vs the best library per shape)
 #   perf       scripts/perf.py time over the BASELINE shapes
-#   pdlab      PDL on/off on latency-bound shapes
+#   pdlab      PDL on/off on latency-bound shapes      dtrace  K2' per-CTA timelines (trace library)
 #   narrow     K2' vs K2 on kv-head shards (Hkv = 1/2/4) and batch 4096     e2e   perf.py e2e breakdown
 set -u
 TAG=$1; shift
@@ -52,6 +52,8 @@ for r in "$@"; do
             done > ${O}_narrow.log 2>&1; cat ${O}_narrow.log ;;
     pdlab) for v in 1 0; do B200ATTN_PDL=$v timeout 600 python scripts/perf.py time --tag pdl$v \
              --shapes C1,d1x512,d1x8k,d4x2k,d16x512,d64x512,C2; done > ${O}_pdlab.log 2>&1; cat ${O}_pdlab.log ;;
+    dtrace) B200ATTN_LIB=$PWD/paper_2505_03780_b200/_lib/libb200attn_trace.so timeout 600 python scripts/perf.py \
+             dtrace --shapes d64x512,d16x512,d1x8k,C2,C4kv1,C2kv2 > ${O}_dtrace.log 2>&1; cat ${O}_dtrace.log ;;
     e2e) timeout 600 python scripts/perf.py e2e > ${O}_e2e.log 2>&1; cat ${O}_e2e.log ;;
     *) echo "unknown recipe $r" >&2 ;;
   esac

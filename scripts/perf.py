@@ -8,6 +8,7 @@
   perf.py trace   [BLOCK_M num_stages num_warps]                 -- clock64 trace (needs a -DB200_TRACE build)
   perf.py umma-rate                                              -- tcgen05 MMA issue-rate probe
   perf.py e2e                                                    -- e2e decode step breakdown (C2)
+  perf.py dtrace --shapes d64x512                                -- K2' per-CTA timeline (trace build)
 """
 
 from __future__ import annotations
@@ -96,7 +97,7 @@ def cmd_time(a):
             try:
                 p, work, sc, unit = make_plan(op, shape, cfg)
                 reps = a.reps or (200 if name == "C1" else 10)
-                ms = graph_ms(p.run, reps)
+                ms = graph_ms(p.run_partial if a.partial else p.run, reps)
                 print(json.dumps({"tag": a.tag, "shape": name, "cfg": p.config, "us": ms * 1e3,
                                   unit: work / (ms / 1e3) / sc}), flush=True)
                 del p
@@ -177,6 +178,36 @@ def cmd_umma_rate(a):
         print(f"{name:34s}: {cyc:7.1f} cycles / 8 MMAs (floor {ideal:.0f}) -> {ideal / cyc * 100:.0f}% of floor")
 
 
+def cmd_dtrace(a):
+    """K2' per-CTA timeline (needs the -DB200_TRACE library: B200ATTN_LIB=.../libb200attn_trace.so):
+    %globaltimer stamps per CTA -> per event the min / median / max offset from the earliest entry."""
+    import numpy as np
+
+    lib = _native.load()
+    lib.b200attn_debug_dtrace.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    names = ["entry", "scan", "first_S", "last_P", "out_written", "merged", "exit"]
+    for name in a.shapes.split(","):
+        op, shape = SHAPES[name]
+        p, *_ = make_plan(op, shape, json.loads(a.cfg) if a.cfg else None)
+        for _ in range(5):
+            p.run()
+        torch.cuda.synchronize()
+        buf = (ctypes.c_ulonglong * (1024 * 8))()
+        lib.b200attn_debug_dtrace(buf, 1024 * 8)
+        t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8).astype(np.int64)
+        n = int(p.num_splits) if p.config.get("TILE_N") == 16 else 0
+        t = t[:n] if n else t[:148]
+        t0 = t[:, 0].min()
+        rel = (t - t0) / 1e3  # us
+        out = {"tag": a.tag, "shape": name, "cfg": p.config, "ctas": int(len(t))}
+        for k, nm in enumerate(names):
+            col = rel[:, k]
+            col = col[(t[:, k] > 0)]
+            if len(col):
+                out[nm] = [round(float(col.min()), 2), round(float(np.median(col)), 2), round(float(col.max()), 2)]
+        print(json.dumps(out), flush=True)
+
+
 def cmd_e2e(a):
     """Where the e2e decode step's time goes (C2): device-only plan, the copies alone, append alone,
     and attention.DecodeStep (one graph: H2D -> append -> decode -> D2H) at several chunk counts."""
@@ -223,17 +254,18 @@ def cmd_e2e(a):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("cmd", choices=["time", "single", "prof", "trace", "umma-rate", "e2e"])
+    ap.add_argument("cmd", choices=["time", "single", "prof", "trace", "umma-rate", "e2e", "dtrace"])
     ap.add_argument("args", nargs="*")
     ap.add_argument("--op", default="prefill")
     ap.add_argument("--shapes", default="C3")
     ap.add_argument("--cfg", default=None)
     ap.add_argument("--all-variants", action="store_true")
     ap.add_argument("--reps", type=int, default=0)
+    ap.add_argument("--partial", action="store_true", help="decode: time K2 / K2' alone (no combine)")
     ap.add_argument("--n", type=int, default=3)
     ap.add_argument("--tag", default="")
     a = ap.parse_args()
-    {"time": cmd_time, "single": cmd_single, "prof": cmd_prof, "trace": cmd_trace, "umma-rate": cmd_umma_rate, "e2e": cmd_e2e}[a.cmd](a)
+    {"time": cmd_time, "single": cmd_single, "prof": cmd_prof, "trace": cmd_trace, "umma-rate": cmd_umma_rate, "e2e": cmd_e2e, "dtrace": cmd_dtrace}[a.cmd](a)
 
 
 if __name__ == "__main__":
