@@ -90,7 +90,8 @@ struct FlatCfg {
 
 #ifdef B200_TRACE
 // debug-only per-CTA timeline (%globaltimer ns): 0 entry, 1 after the tile scan, 2 first S seen by the
-// softmax, 3 last P of the range, 4 last segment's output / partial written, 5 merge done, 6 exit
+// softmax, 3 last P of the range, 4 last segment's output / partial written, 7 arrival counted (fused
+// merge), 5 merge done, 6 exit
 __device__ unsigned long long g_dtrace[1024][8];
 __device__ __forceinline__ void dtrace(int ev) {
   unsigned long long t;
@@ -159,6 +160,7 @@ __device__ __forceinline__ void flat_merge_if_last(const FlatDecodeArgs& args, c
     flags[10] = c1;
   }
   named_bar_sync(1, 128);
+  DTRACE(7, row == 0);
   if (!flags[8]) return;
   __threadfence();
   const int c0 = flags[9], c1 = flags[10], self = static_cast<int>(blockIdx.x);

@@ -13,6 +13,7 @@
 #   sota       scripts/sota.py (same-box library comparators)   single    single-launch vs amortised
 #   sotagrid   scripts/sota.py --grid (C5 grid, relative_cdf vs the best library per shape)
 #   perf       scripts/perf.py time over the BASELINE shapes
+#   flatsweep  K2' CTA count (min tiles per CTA) x fused/K3' merge on small decode shapes
 #   pdlab      PDL on/off on latency-bound shapes      dtrace  K2' per-CTA timelines (trace library)
 #   narrow     K2' vs K2 on kv-head shards (Hkv = 1/2/4) and batch 4096     e2e   perf.py e2e breakdown
 set -u
@@ -54,6 +55,11 @@ for r in "$@"; do
              --shapes C1,d1x512,d1x8k,d4x2k,d16x512,d64x512,C2; done > ${O}_pdlab.log 2>&1; cat ${O}_pdlab.log ;;
     dtrace) B200ATTN_LIB=$PWD/paper_2505_03780_b200/_lib/libb200attn_trace.so timeout 600 python scripts/perf.py \
              dtrace --shapes d64x512,d16x512,d1x8k,C2,C4kv1,C2kv2 > ${O}_dtrace.log 2>&1; cat ${O}_dtrace.log ;;
+    flatsweep) for mt in 2 4 8 16; do for fm in auto 0; do
+               env B200ATTN_FLAT_MIN_TILES=$mt $( [ $fm = 0 ] && echo B200ATTN_FLAT_MERGE=0 ) timeout 300 python scripts/perf.py time \
+                 --tag "mt$mt-merge$fm" --shapes d1x512,d1x8k,d4x2k,d16x512,d64x512,C2kv2,C2kv1 \
+                 --cfg '{"TILE_N": 16, "num_splits": 0, "num_stages": 4}'; done; done > ${O}_flatsweep.log 2>&1
+               cat ${O}_flatsweep.log ;;
     e2e) timeout 600 python scripts/perf.py e2e > ${O}_e2e.log 2>&1; cat ${O}_e2e.log ;;
     *) echo "unknown recipe $r" >&2 ;;
   esac

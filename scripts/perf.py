@@ -185,7 +185,7 @@ def cmd_dtrace(a):
 
     lib = _native.load()
     lib.b200attn_debug_dtrace.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    names = ["entry", "scan", "first_S", "last_P", "out_written", "merged", "exit"]
+    names = ["entry", "scan", "first_S", "last_P", "out_written", "merged", "exit", "arrived"]
     for name in a.shapes.split(","):
         op, shape = SHAPES[name]
         p, *_ = make_plan(op, shape, json.loads(a.cfg) if a.cfg else None)
