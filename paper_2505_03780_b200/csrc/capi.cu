@@ -445,6 +445,16 @@ bool flat_fused_merge(int batch, int ctas) {
   return ctas <= 8 * batch;
 }
 
+// K3' launched with PDL behind a late-triggering K2' (B200ATTN_PDL_COMBINE=1; A/B)
+bool flat_pdl_combine() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("B200ATTN_PDL_COMBINE");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 using FlatLauncher = int (*)(const b200attn_decode_params*, bool combine, cudaStream_t);
 
 template <int HKV, int G, int NS, bool FP8>
@@ -483,6 +493,8 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
   a.part_ml = a.part_o + slots * p->num_q_heads * 128;
   a.cu_tiles_out = reinterpret_cast<int32_t*>(a.part_ml + slots * p->num_q_heads * 2);
   const bool fused = flat_fused_merge(p->batch, ctas);
+  const bool pdl_combine = combine && !fused && pdl_enabled() && flat_pdl_combine();
+  a.late_trigger = pdl_combine ? 1 : 0;
   a.seq_cnt = fused ? counters : nullptr;
   a.batch = p->batch;
   a.block_size = p->block_size;
@@ -497,11 +509,17 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
   cudaError_t e = launch_k(kern, dim3(ctas), dim3(C::NTHREADS), smem, stream, mq, mk, mv, a);
   if (e != cudaSuccess) return cuda_fail(e, "decode_flat launch");
   if (combine && !fused) {
-    // a plain launch: with PDL its CTAs became resident beside K2' and the 1-sequence x 8k decode lost
-    // 6 us (22.1 vs 15.9 us, r2d pdlab); K2' of the next step still overlaps this kernel's tail
-    b200::flat_combine_kernel<C::NQ><<<dim3(p->batch, C::NQ), 128, 0, stream>>>(
-        a.part_o, a.part_ml, a.cu_tiles_out, p->batch, ctas, reinterpret_cast<__nv_bfloat16*>(p->o));
-    e = cudaGetLastError();
+    if (pdl_combine) {  // K2' triggers late, so K3' becomes resident only in K2's tail
+      e = launch_k(b200::flat_combine_kernel<C::NQ>, dim3(p->batch, C::NQ), dim3(128), 0, stream,
+                   (const float*)a.part_o, (const float*)a.part_ml, (const int32_t*)a.cu_tiles_out, (int)p->batch,
+                   ctas, reinterpret_cast<__nv_bfloat16*>(p->o));
+    } else {
+      // a plain launch: PDL-launched while K2' triggered at its start, its CTAs sat resident beside
+      // K2' and the 1-sequence x 8k decode lost 6 us (22.1 vs 15.9 us, r2d pdlab)
+      b200::flat_combine_kernel<C::NQ><<<dim3(p->batch, C::NQ), 128, 0, stream>>>(
+          a.part_o, a.part_ml, a.cu_tiles_out, p->batch, ctas, reinterpret_cast<__nv_bfloat16*>(p->o));
+      e = cudaGetLastError();
+    }
     if (e != cudaSuccess) return cuda_fail(e, "flat combine launch");
   }
   return B200ATTN_OK;

@@ -47,6 +47,8 @@ struct FlatDecodeArgs {
   int32_t max_blocks;
   float scale_log2;  // softmax_scale * log2(e)  (fp8: * k_scale)
   float out_scale;   // 1                        (fp8: v_scale)
+  int32_t late_trigger;  // PDL: 0 = let the next kernel launch at once; 1 = once this CTA's tile loops end
+                         // (a PDL-launched K3' then becomes resident only in K2's tail)
 };
 
 template <int HKV_, int G, int NSTAGE, bool FP8 = false>
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
     tma_prefetch_desc(&tmap_v);
   }
   griddep_wait();  // PDL: the prologue above overlapped the previous kernel; data access starts here
-  griddep_launch();
+  if (!args.late_trigger) griddep_launch();
   // ---- tiles per sequence -> cu (exclusive prefix), block-wide: each thread scans a contiguous
   // chunk of sequences (any batch size, no serial chain of loads)
   {
@@ -746,6 +748,7 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
     }
   }
 
+  if (args.late_trigger) griddep_launch();
   tc_fence_before();
   __syncthreads();
   if (warp == C::MMA_WARP) {

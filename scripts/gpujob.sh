@@ -13,6 +13,7 @@
 #   sota       scripts/sota.py (same-box library comparators)   single    single-launch vs amortised
 #   sotagrid   scripts/sota.py --grid (C5 grid, relative_cdf vs the best library per shape)
 #   perf       scripts/perf.py time over the BASELINE shapes
+#   mergeab    K2' fused merge vs K3' (plain / PDL behind a late trigger) on the decode shapes
 #   flatsweep  K2' CTA count (min tiles per CTA) x fused/K3' merge on small decode shapes
 #   pdlab      PDL on/off on latency-bound shapes      dtrace  K2' per-CTA timelines (trace library)
 #   narrow     K2' vs K2 on kv-head shards (Hkv = 1/2/4) and batch 4096     e2e   perf.py e2e breakdown
@@ -60,6 +61,10 @@ for r in "$@"; do
                  --tag "mt$mt-merge$fm" --shapes d1x512,d1x8k,d4x2k,d16x512,d64x512,C2kv2,C2kv1 \
                  --cfg '{"TILE_N": 16, "num_splits": 0, "num_stages": 4}'; done; done > ${O}_flatsweep.log 2>&1
                cat ${O}_flatsweep.log ;;
+    mergeab) for v in "" "B200ATTN_FLAT_MERGE=0" "B200ATTN_FLAT_MERGE=0 B200ATTN_PDL_COMBINE=1" "B200ATTN_PDL_COMBINE=1" \
+                 "B200ATTN_FLAT_MERGE=0 B200ATTN_PDL_COMBINE=1 B200ATTN_FLAT_MIN_TILES=4"; do
+               env $v timeout 300 python scripts/perf.py time --tag "[$v]" --shapes C2,C4shard,C2fp8,d64x512,d1x8k,d16x512,C2kv2,C4kv1
+             done > ${O}_mergeab.log 2>&1; cat ${O}_mergeab.log ;;
     e2e) timeout 600 python scripts/perf.py e2e > ${O}_e2e.log 2>&1; cat ${O}_e2e.log ;;
     *) echo "unknown recipe $r" >&2 ;;
   esac
