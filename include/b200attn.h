@@ -127,8 +127,10 @@ size_t b200attn_prefill_workspace_size(const b200attn_prefill_params* p);
 int b200attn_prefill(const b200attn_prefill_params* p, const b200attn_prefill_variant* v, void* stream);
 
 /* K2 (+K3): paged split-KV decode; the combine runs iff the resolved num_splits > 1.  tile_n 16 (K2'):
- * split sequences are merged inside K2' by the CTA finishing their last piece when sequences span few
- * CTAs (batch >= ~num_SMs / 8), else by the K3' combine launch. */
+ * sequences split between CTAs are merged by the K3' combine launch (an in-kernel merge by the CTA
+ * finishing a sequence's last piece is kept behind B200ATTN_FLAT_MERGE=1).  Kernels are launched with
+ * programmatic dependent launch (B200ATTN_PDL=0 disables it): a kernel's prologue may overlap the
+ * previous kernel in the stream, and no kernel touches global memory before that one completed. */
 size_t b200attn_decode_workspace_size(const b200attn_decode_params* p, const b200attn_decode_variant* v);
 int b200attn_decode_num_splits(const b200attn_decode_params* p, const b200attn_decode_variant* v);
 /* Number of kernels b200attn_decode enqueues for this shape and config (1 or 2), or -1 if invalid. */

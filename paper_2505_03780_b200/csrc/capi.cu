@@ -404,12 +404,12 @@ int num_sms() {  // per device (cached; a process may drive several GPUs)
 
 // Persistent CTAs, but at least flat_min_tiles() tiles each when the (host-known upper bound of the)
 // tile count is small: fewer partial segments to merge, same memory parallelism.
-// B200ATTN_FLAT_MIN_TILES overrides the default 2 (A/B).
+// B200ATTN_FLAT_MIN_TILES overrides the default 4 (A/B).
 int flat_min_tiles() {
   static int v = 0;
   if (v == 0) {
     const char* e = getenv("B200ATTN_FLAT_MIN_TILES");
-    v = (e && atoi(e) > 0) ? atoi(e) : 2;
+    v = (e && atoi(e) > 0) ? atoi(e) : 4;  // 4: 1 x 8k 13.9 vs 16.0 us, 16 x 512 12.6 vs 13.0 (r2f/r2g)
   }
   return v;
 }
@@ -431,9 +431,12 @@ size_t flat_workspace_bytes(const b200attn_decode_params* p) {
          ((size_t)p->batch + 1) * sizeof(int32_t);
 }
 
-// Merge split sequences inside K2' (last-arriving piece, no K3' launch) when sequences span few
-// CTAs: with ~ctas / B + 1 pieces each, the merging CTA reads a handful of partials at its tail.
-// B200ATTN_FLAT_MERGE=0/1 forces either path (A/B).
+// Merge split sequences inside K2' (the CTA finishing a sequence's last piece merges it, no K3'
+// launch) only when asked (B200ATTN_FLAT_MERGE=1, with sequences spanning few CTAs).  Measured
+// against the parallel K3' on the same build (r2g mergeab, us): C2 162.8 vs 159.0, C4 shard 653 vs
+// 632, 64 x 512 36.7 vs 32.4, C2 at Hkv = 2 52.8 vs 50.5 — the merging CTAs' fence + atomic + L2
+// reads sit in the kernel's tail (trace: up to 8 us after the last P) while K3' reduces every
+// (sequence, q head) in parallel once streaming is done.
 bool flat_fused_merge(int batch, int ctas) {
   static int force = -2;
   if (force == -2) {
@@ -441,8 +444,7 @@ bool flat_fused_merge(int batch, int ctas) {
     force = (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : -1;
   }
   if (batch > (int)kFlatCounters) return false;  // the arrival counters cover the first 1024 sequences
-  if (force >= 0) return force == 1;
-  return ctas <= 8 * batch;
+  return force == 1 && ctas <= 8 * batch;
 }
 
 // K3' launched with PDL behind a late-triggering K2' (B200ATTN_PDL_COMBINE=1; A/B)

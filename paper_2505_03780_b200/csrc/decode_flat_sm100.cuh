@@ -545,9 +545,10 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
       for (; t < seg_end; ++t, ++i) {
         const int sb = i & 1;
         mbar_wait(&s_full[sb], (i >> 1) & 1);
-        // observe every phase of o_full (compute-sanitizer synccheck): PV(i-2) was issued before
-        // QK(i) and tcgen05 ops complete in order, so this wait returns at once
-        if (i >= 2) mbar_wait(&o_full[(i - 2) & 1], ((i - 2) >> 1) & 1);
+        // every phase of o_full is observed (compute-sanitizer synccheck): PV(i-2) was issued before
+        // QK(i) and tcgen05 ops complete in order, so the phase is complete; probed here, waited on
+        // (never in practice) before P(i) is handed over, while PV(i) cannot have been issued
+        const bool of_seen = i < 2 || mbar_test(&o_full[(i - 2) & 1], ((i - 2) >> 1) & 1);
         tc_fence_after();
         DTRACE(2, row == 0 && i == 0);
         const int tok = (t - tile0) * C::TT + pch * 16 + t16;
@@ -675,6 +676,7 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
         }
         fence_proxy_async_smem();
         tc_fence_before();
+        if (!of_seen) mbar_wait(&o_full[(i - 2) & 1], ((i - 2) >> 1) & 1);
         mbar_arrive(&p_full[sb]);
         DTRACE(3, row == 0 && t == T1 - 1);
       }

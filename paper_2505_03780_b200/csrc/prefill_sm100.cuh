@@ -530,6 +530,15 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
     const uint32_t pair_bar = 1 + t * 4 + (warp & 3);
     auto xidx = [&](int k, int h) { return ((k * NQ + t) * SPLIT + h) * 128 + row; };
     const float sl2 = args.scale_log2;
+    // every phase of o_done is observed (compute-sanitizer synccheck): PV_t(g - LA) was issued before
+    // QK_t(g) and tcgen05 ops complete in order, so once S_t(g) was seen the phase is complete.  It is
+    // probed (non-blocking) right after S_t(g) and, in the never-taken case, waited on before P_t(g)
+    // is handed over — while PV_t(g), the barrier's next phase at LA = 2, cannot have been issued
+    auto o_done_bar = [&](int g) { return &o_done[2 * t + ((g - C::LA) & 1)]; };
+    auto o_done_par = [&](int g) { return static_cast<uint32_t>(((g - C::LA) >> 1) & 1); };
+    auto observe_o_done = [&](int g, bool seen) {
+      if (g >= C::LA && !seen) mbar_wait(o_done_bar(g), o_done_par(g));
+    };
     int gt = 0;
     for (int k = 0;; ++k) {
       mbar_wait(&item_full[k & 1], (k >> 1) & 1);
@@ -549,9 +558,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
       for (int j = 0; j < n_kv; ++j) {
         const int buf = (gt + j) % C::SB;
         mbar_wait(&s_full[t * C::SB + buf], ((gt + j) / C::SB) & 1);
-        // observe every phase of o_done (compute-sanitizer synccheck): PV_t(g - LA) was issued before
-        // QK_t(g) and tcgen05 ops complete in order, so this wait returns at once
-        if (gt + j >= C::LA) mbar_wait(&o_done[2 * t + ((gt + j - C::LA) & 1)], ((gt + j - C::LA) >> 1) & 1);
+        const bool od_seen = gt + j < C::LA || mbar_test(o_done_bar(gt + j), o_done_par(gt + j));
         tc_fence_after();
         const uint32_t s_addr = s_base + C::S_COL(t, buf);
         if (row == 0 && hh == 0) TRACE(t, gt + j);
@@ -571,6 +578,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
           tc_fence_before();
           if (row == 0 && hh == 0) TRACE(2 + t, gt + j);
           if (t == 0 && lane == 0 && warp < 4) TRACE(8 + warp, gt + j);
+          observe_o_done(gt + j, od_seen);
           mbar_arrive(&p_full[2 * t + ((gt + j) & 1)]);
           continue;
         }
@@ -615,6 +623,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
         tc_fence_before();
         if (row == 0 && hh == 0) TRACE(2 + t, gt + j);
         if (t == 0 && lane == 0 && warp < 4) TRACE(8 + warp, gt + j);
+        observe_o_done(gt + j, od_seen);
         mbar_arrive(&p_full[2 * t + ((gt + j) & 1)]);
       }
 

@@ -700,3 +700,33 @@ def test_runner_b200_backend_end_to_end():
     p.stdin.write(json.dumps({"type": "shutdown"}) + "\n")
     p.stdin.flush()
     assert p.wait(timeout=30) == 0
+
+
+def test_decode_flat_fused_merge_option(tmp_path):
+    """The in-kernel merge (B200ATTN_FLAT_MERGE=1, read once per process -> a subprocess): 64 ragged
+    sequences split across 2-3 CTAs each, merged by the CTA finishing their last piece; vs the oracle."""
+    script = tmp_path / "fused.py"
+    script.write_text(
+        "import sys, torch\n"
+        f"sys.path.insert(0, {str(ROOT)!r})\n"
+        "from paper_2505_03780_b200 import attention as A, workload as W\n"
+        "g = torch.Generator().manual_seed(21)\n"
+        "lens = torch.randint(1, 3000, (64,), generator=g).tolist(); lens[3] = 0\n"
+        "d = W.make_decode(dict(W.C2, batch_size=64, seq_len=max(lens)), device='cpu', lens=lens, extra_blocks=4)\n"
+        "args = [t.cuda() for t in (d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)]\n"
+        "p = A.DecodePlan(*args, config=dict(num_splits=0, num_stages=4, TILE_N=16))\n"
+        "assert p.kernels_per_run() == 1, p.kernels_per_run()\n"
+        f"torch.save(dict(out=p.run().cpu(), lens=lens), {str(tmp_path / 'out.pt')!r})\n")
+    env = dict(os.environ, B200ATTN_FLAT_MERGE="1")
+    r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = torch.load(tmp_path / "out.pt")
+    lens = res["lens"]
+    d = W.make_decode(dict(W.C2, batch_size=64, seq_len=max(lens)), device="cpu", lens=lens, extra_blocks=4)
+    assert res["out"][3].abs().max().item() == 0
+    sub = [0, 1, 2, 40, 63]
+    ref = oracle.decode(d.q[sub], d.k_cache, d.v_cache, d.block_table[sub], d.seq_lens[sub])
+    args = [t.to(DEV) for t in (d.q, d.k_cache, d.v_cache, d.block_table, d.seq_lens)]
+    ki = torch.tensor(sub, device=DEV)
+    check("decode flat fused in-kernel merge", res["out"][sub], ref,
+          sdpa_decode_bf16(args[0][ki], args[1], args[2], args[3][ki], args[4][ki]))
