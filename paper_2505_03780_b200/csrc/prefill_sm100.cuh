@@ -104,11 +104,7 @@ struct PrefillCfg {
   static constexpr int LA = SB;                                       // QK lookahead (KV steps)
   // q_full[2], q_empty[2], kv_full/empty[NSLOT], s_full[NQ][SB], p_full[NQ][2], o_done[NQ][2],
   // o_free[NQ], item_full/empty[2]
-  // HP (BLOCK_N = 128, one thread per row): P is handed to the PV MMA in two 64-key halves —
-  // PV over keys 0..63 runs while the softmax computes keys 64..127.  p_lo_full[NQ][2] (P of keys
-  // 0..63 written, per step parity) and o_lo_done[NQ][2] (that half-PV landed) follow item_empty.
-  static constexpr bool HP = (BN == 128 && SPLIT == 1);
-  static constexpr int NUM_BARS = 4 + 2 * NSLOT + NQ * SB + 2 * NQ + 2 * NQ + NQ + 4 + 4 * NQ;
+  static constexpr int NUM_BARS = 4 + 2 * NSLOT + NQ * SB + 2 * NQ + 2 * NQ + NQ + 4;
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
   static constexpr uint32_t TMEM_COLS = 512;
   __host__ __device__ static constexpr uint32_t S_COL(int t, int b) { return (t * SB + b) * BN; }
@@ -176,19 +172,19 @@ __device__ __forceinline__ void prefill_decode_item(int w, const PrefillKernelAr
 // Pass 2 over one S row: P = exp2(S*sl2 - m) -> bf16 pairs written back over the S columns;
 // returns the row sum.  MASKED is a compile-time split so the common (interior) tile carries no
 // per-element compare/select at all — predicated-off instructions still cost issue slots.
-template <int BN, bool MASKED, int EMU, int C0 = 0, int C1 = BN / 32>  // 32-column chunks [C0, C1)
+template <int BN, bool MASKED, int EMU>
 __device__ __forceinline__ float softmax_pass2(uint32_t s_addr, float sl2, float nmu, int kv0, int lim) {
   // four independent FADD2 accumulators: a single running sum is a 64-deep dependent chain;
   // 32-column chunks with the next chunk's tcgen05.ld in flight (P of chunk c lands on S
   // columns [16c, 16c + 16), all of which were loaded before)
   float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   uint32_t r[2][32];
-  tmem_ld32_nowait(s_addr + C0 * 32, r[C0 & 1]);
-  tmem_wait_ld_regs(r[C0 & 1]);
+  tmem_ld32_nowait(s_addr, r[0]);
+  tmem_wait_ld_regs(r[0]);
 #pragma unroll
-  for (int c = C0; c < C1; ++c) {
+  for (int c = 0; c < BN / 32; ++c) {
     uint32_t(&cur)[32] = r[c & 1];
-    if (c + 1 < C1) tmem_ld32_nowait(s_addr + (c + 1) * 32, r[(c + 1) & 1]);
+    if (c + 1 < BN / 32) tmem_ld32_nowait(s_addr + (c + 1) * 32, r[(c + 1) & 1]);
     uint32_t pk[16];
     const int col0 = kv0 + c * 32;
 #pragma unroll
@@ -215,7 +211,7 @@ __device__ __forceinline__ float softmax_pass2(uint32_t s_addr, float sl2, float
       fadd2(ls[acc], ls[acc + 1], e0, e1);
       pk[i >> 1] = pack_bf16x2(e0, e1);
     }
-    if (c + 1 < C1) tmem_wait_ld_regs(r[(c + 1) & 1]);
+    if (c + 1 < BN / 32) tmem_wait_ld_regs(r[(c + 1) & 1]);
     tmem_st16(s_addr + c * 16, pk);  // P overwrites S columns this thread has already read
   }
   fadd2(ls[0], ls[1], ls[2], ls[3]);
@@ -224,17 +220,17 @@ __device__ __forceinline__ float softmax_pass2(uint32_t s_addr, float sl2, float
   return ls[0] + ls[1];
 }
 
-template <int BN, bool MASKED, int C0 = 0, int C1 = BN / 32>  // 32-column chunks [C0, C1)
+template <int BN, bool MASKED>
 __device__ __forceinline__ float softmax_rowmax(uint32_t s_addr, int kv0, int lim) {
   // four independent 3-input max chains (FMNMX3); all chunk loads in flight before one wait
   float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
   uint32_t r[2][32];
-  tmem_ld32_nowait(s_addr + C0 * 32, r[C0 & 1]);
-  tmem_wait_ld_regs(r[C0 & 1]);
+  tmem_ld32_nowait(s_addr, r[0]);
+  tmem_wait_ld_regs(r[0]);
 #pragma unroll
-  for (int c = C0; c < C1; ++c) {
+  for (int c = 0; c < BN / 32; ++c) {
     uint32_t(&cur)[32] = r[c & 1];
-    if (c + 1 < C1) tmem_ld32_nowait(s_addr + (c + 1) * 32, r[(c + 1) & 1]);
+    if (c + 1 < BN / 32) tmem_ld32_nowait(s_addr + (c + 1) * 32, r[(c + 1) & 1]);
 #pragma unroll
     for (int i = 0; i < 32; i += 2) {
       float a0 = __uint_as_float(cur[i]), a1 = __uint_as_float(cur[i + 1]);
@@ -246,7 +242,7 @@ __device__ __forceinline__ float softmax_rowmax(uint32_t s_addr, int kv0, int li
       const int k = (i >> 1) & 3;
       m[k] = fmaxf(m[k], fmaxf(a0, a1));
     }
-    if (c + 1 < C1) tmem_wait_ld_regs(r[(c + 1) & 1]);
+    if (c + 1 < BN / 32) tmem_wait_ld_regs(r[(c + 1) & 1]);
   }
   return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
 }
@@ -303,49 +299,6 @@ __device__ __forceinline__ bool softmax_speculative(uint32_t s_addr, float sl2, 
   return true;
 }
 
-// Half of a 128-column interior tile (chunks [C0, C0 + 2)) in the speculative single pass: P of
-// these 64 keys is stored (over S columns [16 C0, 16 C0 + 32), already read) only if no row sum of
-// the warp passed 2^64 — so the caller can hand each half to the PV MMA as soon as it is ready.
-template <int EMU, int C0>
-__device__ __forceinline__ bool softmax_spec_half(uint32_t s_addr, float sl2, float m_run, float& lsum) {
-  float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  uint32_t pk[32];
-  const float nmu = -m_run;
-  uint32_t r[2][32];
-  tmem_ld32_nowait(s_addr + C0 * 32, r[0]);
-  tmem_wait_ld_regs(r[0]);
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    uint32_t(&cur)[32] = r[c];
-    if (c == 0) tmem_ld32_nowait(s_addr + (C0 + 1) * 32, r[1]);
-#pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-      const int k = (i >> 1) & 3;
-      float x0, x1;
-      ffma2(x0, x1, __uint_as_float(cur[i]), __uint_as_float(cur[i + 1]), sl2, nmu);
-      float e0, e1;
-      if (EMU > 0 && (i >> 1) % EMU == EMU - 1) {
-        exp2_poly2<true>(x0, x1, e0, e1);
-      } else {
-        e0 = fast_exp2(x0);
-        e1 = fast_exp2(x1);
-      }
-      fadd2(ls[2 * k], ls[2 * k + 1], e0, e1);
-      pk[(c * 32 + i) >> 1] = pack_bf16x2(e0, e1);
-    }
-    if (c == 0) tmem_wait_ld_regs(r[1]);
-  }
-  fadd2(ls[0], ls[1], ls[2], ls[3]);
-  fadd2(ls[4], ls[5], ls[6], ls[7]);
-  fadd2(ls[0], ls[1], ls[4], ls[5]);
-  lsum = ls[0] + ls[1];
-  const bool ok = m_run != -INFINITY && lsum <= 1.8446744e19f;  // 2^64
-  if (!__all_sync(0xffffffffu, ok)) return false;
-  tmem_st16(s_addr + C0 * 16, *reinterpret_cast<const uint32_t(*)[16]>(pk));
-  tmem_st16(s_addr + C0 * 16 + 16, *reinterpret_cast<const uint32_t(*)[16]>(pk + 16));
-  return true;
-}
-
 #ifdef B200_TRACE
 // debug-only event trace of CTA 0: [event][slot] clock64 stamps
 __device__ unsigned long long g_trace[16][512];  // 8..11: P done by warp 0..3 of tile 0; 12..15: S seen
@@ -385,8 +338,6 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
   uint64_t* o_free = o_done + 2 * NQ;      // [NQ]      epilogue of O_t done (128 arrivals)
   uint64_t* item_full = o_free + NQ;       // [2]
   uint64_t* item_empty = item_full + 2;
-  uint64_t* p_lo_full = item_empty + 2;    // [NQ][2]   (HP) P_t of keys 0..63 of a step of that parity
-  uint64_t* o_lo_done = p_lo_full + 2 * NQ;  // [NQ][2] (HP) PV_t over keys 0..63 of that step landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS);
 
   const int warp = warp_id();
@@ -408,10 +359,6 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
       mbar_init(&o_done[2 * t], 1);
       mbar_init(&o_done[2 * t + 1], 1);
       mbar_init(&o_free[t], C::TILE_THREADS);
-      for (int b = 0; b < 2; ++b) {
-        mbar_init(&p_lo_full[2 * t + b], C::TILE_THREADS);
-        mbar_init(&o_lo_done[2 * t + b], 1);
-      }
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&item_full[i], 1);
@@ -501,11 +448,6 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
         const uint64_t kb = k_desc + ((slot * C::KV_BYTES) >> 4);
         umma_ss_k128<2, C::HALF_Q / 16, 2, C::HALF_KV / 16>(tmem + C::S_COL(t, buf), qa, kb, IDESC_QK, 0u);
       };
-      // HP: PV over keys [64 h, 64 h + 64): A = P columns [32 h, 32 h + 32) of S_t, B = that half of V
-      auto issue_pv_half = [&](int t, int slot, int buf, int h, bool acc) {
-        const uint64_t vb = v_desc + ((slot * C::KV_BYTES) >> 4) + h * 512;
-        umma_ts_k64<128>(tmem + C::O_COL(t), tmem + C::S_COL(t, buf) + h * 32, vb, IDESC_PV, acc ? 1u : 0u);
-      };
       auto issue_pv = [&](int t, int slot, int buf, bool acc) {
         const uint64_t vb = v_desc + ((slot * C::KV_BYTES) >> 4);
         if constexpr (BN == 128) {
@@ -555,26 +497,12 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
           mbar_wait_producer(&kv_full[vslot], (vi / NS) & 1);
           TRACE(6, gt + j);
           for (int t = 0; t < NQ; ++t) {
-            const int par = (gt + j) & 1;
-            const uint32_t ph = ((gt + j) >> 1) & 1;
-            if constexpr (C::HP) {
-              mbar_wait_producer(&p_lo_full[2 * t + par], ph);
-              if (j == 0 && k > 0) mbar_wait_producer(&o_free[t], (k - 1) & 1);
-              tc_fence_after();
-              issue_pv_half(t, vslot, (gt + j) % SB, 0, j > 0);
-              umma_commit_w(&o_lo_done[2 * t + par]);
-              mbar_wait_producer(&p_full[2 * t + par], ph);
-              TRACE(4 + t, gt + j);
-              tc_fence_after();
-              issue_pv_half(t, vslot, (gt + j) % SB, 1, true);
-            } else {
-              mbar_wait_producer(&p_full[2 * t + par], ph);
-              TRACE(4 + t, gt + j);
-              if (j == 0 && k > 0) mbar_wait_producer(&o_free[t], (k - 1) & 1);
-              tc_fence_after();
-              issue_pv(t, vslot, (gt + j) % SB, j > 0);
-            }
-            umma_commit_w(&o_done[2 * t + par]);
+            mbar_wait_producer(&p_full[2 * t + ((gt + j) & 1)], ((gt + j) >> 1) & 1);
+            TRACE(4 + t, gt + j);
+            if (j == 0 && k > 0) mbar_wait_producer(&o_free[t], (k - 1) & 1);
+            tc_fence_after();
+            issue_pv(t, vslot, (gt + j) % SB, j > 0);
+            umma_commit_w(&o_done[2 * t + ((gt + j) & 1)]);
             if (t == NQ - 1) umma_commit_w(&kv_empty[vslot]);
             if (j + LA < n_kv) {
               qk_step_tile(j + LA, t);
@@ -611,12 +539,6 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
     auto observe_o_done = [&](int g, bool seen) {
       if (g >= C::LA && !seen) mbar_wait(o_done_bar(g), o_done_par(g));
     };
-    // HP: the same for o_lo_done (PV_t over keys 0..63 of step g - LA), consumed before P_t of keys
-    // 0..63 of step g is handed over
-    auto o_lo_bar = [&](int g) { return &o_lo_done[2 * t + ((g - C::LA) & 1)]; };
-    auto observe_o_lo = [&](int g, bool seen) {
-      if (g >= C::LA && !seen) mbar_wait(o_lo_bar(g), o_done_par(g));
-    };
     int gt = 0;
     for (int k = 0;; ++k) {
       mbar_wait(&item_full[k & 1], (k >> 1) & 1);
@@ -637,7 +559,6 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
         const int buf = (gt + j) % C::SB;
         mbar_wait(&s_full[t * C::SB + buf], ((gt + j) / C::SB) & 1);
         const bool od_seen = gt + j < C::LA || mbar_test(o_done_bar(gt + j), o_done_par(gt + j));
-        const bool ol_seen = !C::HP || gt + j < C::LA || mbar_test(o_lo_bar(gt + j), o_done_par(gt + j));
         tc_fence_after();
         const uint32_t s_addr = s_base + C::S_COL(t, buf);
         if (row == 0 && hh == 0) TRACE(t, gt + j);
@@ -649,58 +570,8 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
         // function of the rows only, identically for both owners of a row), keep the common path
         // free of per-element compares and selects
         const bool warp_edge = __any_sync(0xffffffffu, edge);
-        // HP: P of keys 0..63 is written -> hand it to the PV MMA (keys 64..127 still being computed)
-        auto hand_lo = [&]() {
-          tmem_wait_st();
-          tc_fence_before();
-          observe_o_lo(gt + j, ol_seen);
-          mbar_arrive(&p_lo_full[2 * t + ((gt + j) & 1)]);
-        };
-        if constexpr (C::HP) {
-          float l0, l1;
-          if (args.speculate && j > 0 && !warp_edge && softmax_spec_half<EMU, 0>(s_addr, sl2, m_run, l0)) {
-            hand_lo();
-            if (!softmax_spec_half<EMU, 2>(s_addr, sl2, m_run, l1)) {
-              // keys 64..127 jumped by > 64 (log2) over the running max: the exact max of that half;
-              // O (PV up to keys 0..63 of this step, all at the old max) is rescaled once that
-              // half-PV has landed, then P of keys 64..127 at the new max
-              const float mt = softmax_rowmax<NCOL, false, 2, 4>(s_addr, kv0h, lim);
-              const float m_new = fmaxf(m_run, mt * sl2);
-              const bool need = (m_new > m_run + 8.0f);
-              float alpha = 1.f;
-              if (need) {
-                alpha = fast_exp2(m_run - m_new);
-                m_run = m_new;
-              }
-              l_run = (l_run + l0) * alpha;
-              l0 = 0.f;
-              if (__any_sync(0xffffffffu, need)) {
-                mbar_wait(&o_lo_done[2 * t + ((gt + j) & 1)], ((gt + j) >> 1) & 1);
-                tc_fence_after();
-#pragma unroll
-                for (int c = 0; c < OCOLS / 32; ++c) {
-                  uint32_t r[32];
-                  tmem_ld32(o_addr + c * 32, r);
-#pragma unroll
-                  for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-                  tmem_st32(o_addr + c * 32, r);
-                }
-              }
-              l1 = softmax_pass2<NCOL, false, EMU, 2, 4>(s_addr, sl2, -m_run, kv0h, lim);
-            }
-            l_run += l0 + l1;
-            tmem_wait_st();
-            tc_fence_before();
-            if (row == 0 && hh == 0) TRACE(2 + t, gt + j);
-            if (t == 0 && lane == 0 && warp < 4) TRACE(8 + warp, gt + j);
-            observe_o_done(gt + j, od_seen);
-            mbar_arrive(&p_full[2 * t + ((gt + j) & 1)]);
-            continue;
-          }
-          // keys 0..63 jumped (or edge / first tile): the exact two-pass path below, nothing handed over
-        }
         float lsum_spec;
-        if (!C::HP && args.speculate && j > 0 && !warp_edge &&
+        if (args.speculate && j > 0 && !warp_edge &&
             softmax_speculative<NCOL, EMU, SPLIT>(s_addr, sl2, m_run, lsum_spec, pair_bar)) {
           l_run += lsum_spec;
           tmem_wait_st();
@@ -745,17 +616,8 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
           }
         }
         const float nmu = (m_run == -INFINITY) ? 0.f : -m_run;
-        float lsum;
-        if constexpr (C::HP) {
-          lsum = warp_edge ? softmax_pass2<NCOL, true, EMU, 0, 2>(s_addr, sl2, nmu, kv0h, lim)
-                           : softmax_pass2<NCOL, false, EMU, 0, 2>(s_addr, sl2, nmu, kv0h, lim);
-          hand_lo();
-          lsum += warp_edge ? softmax_pass2<NCOL, true, EMU, 2, 4>(s_addr, sl2, nmu, kv0h, lim)
-                            : softmax_pass2<NCOL, false, EMU, 2, 4>(s_addr, sl2, nmu, kv0h, lim);
-        } else {
-          lsum = warp_edge ? softmax_pass2<NCOL, true, EMU>(s_addr, sl2, nmu, kv0h, lim)
-                           : softmax_pass2<NCOL, false, EMU>(s_addr, sl2, nmu, kv0h, lim);
-        }
+        const float lsum = warp_edge ? softmax_pass2<NCOL, true, EMU>(s_addr, sl2, nmu, kv0h, lim)
+                                     : softmax_pass2<NCOL, false, EMU>(s_addr, sl2, nmu, kv0h, lim);
         l_run += lsum;
         tmem_wait_st();
         tc_fence_before();

@@ -332,25 +332,6 @@ __device__ __forceinline__ void umma_ts_k128(uint32_t d, uint32_t a_tmem, uint64
       : "memory");
 }
 
-// TS variant over 64 keys (4 K-steps): A from TMEM at a_tmem + 8 kk, B at b + kk * BS (16-B units)
-template <int BS>
-__device__ __forceinline__ void umma_ts_k64(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile("{\n\t.reg .pred e, p;\n\t.reg .b32 ta;\n\t.reg .b64 tb;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
-      "setp.eq.u32 p, 0, 0;\n\t"
-      "add.s32 ta, %1, 8;\n\tadd.s64 tb, %2, %5;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
-      "add.s32 ta, %1, 16;\n\tadd.s64 tb, %2, %6;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
-      "add.s32 ta, %1, 24;\n\tadd.s64 tb, %2, %7;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %3, p;\n\t"
-      "}"
-      :: "r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "n"(BS), "n"(2 * BS), "n"(3 * BS)
-      : "memory");
-}
-
 // Arrive on an mbarrier once every previously issued tcgen05 op of this thread completes.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

@@ -13,8 +13,6 @@
 #   sota       scripts/sota.py (same-box library comparators)   single    single-launch vs amortised
 #   sotagrid   scripts/sota.py --grid (C5 grid, relative_cdf vs the best library per shape)
 #   perf       scripts/perf.py time over the BASELINE shapes
-#   abpf       prefill A/B: _lib/libb200attn_base.so vs the current library (twice, interleaved)
-#   testspf    prefill GPU parity tests only
 #   mergeab    K2' fused merge vs K3' (plain / PDL behind a late trigger) on the decode shapes
 #   flatsweep  K2' CTA count (min tiles per CTA) x fused/K3' merge on small decode shapes
 #   pdlab      PDL on/off on latency-bound shapes      dtrace  K2' per-CTA timelines (trace library)
@@ -67,11 +65,6 @@ for r in "$@"; do
                  "B200ATTN_FLAT_MERGE=0 B200ATTN_PDL_COMBINE=1 B200ATTN_FLAT_MIN_TILES=4"; do
                env $v timeout 300 python scripts/perf.py time --tag "[$v]" --shapes C2,C4shard,C2fp8,d64x512,d1x8k,d16x512,C2kv2,C4kv1
              done > ${O}_mergeab.log 2>&1; cat ${O}_mergeab.log ;;
-    abpf) for i in 1 2; do for L in base cur; do
-            lib=$PWD/paper_2505_03780_b200/_lib/libb200attn.so; [ $L = base ] && lib=$PWD/paper_2505_03780_b200/_lib/libb200attn_base.so
-            B200ATTN_LIB=$lib timeout 300 python scripts/perf.py time --tag "$L$i" --shapes C3,1x16k,4x8k,C1
-          done; done > ${O}_abpf.log 2>&1; cat ${O}_abpf.log ;;
-    testspf) timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -rs -k "prefill or umma" > ${O}_testspf.log 2>&1; tail -15 ${O}_testspf.log ;;
     e2e) timeout 600 python scripts/perf.py e2e > ${O}_e2e.log 2>&1; cat ${O}_e2e.log ;;
     *) echo "unknown recipe $r" >&2 ;;
   esac
