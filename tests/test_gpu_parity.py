@@ -198,17 +198,19 @@ def test_prefill_causal(lens):
 
 @pytest.mark.parametrize("nw", [4, 8])
 @pytest.mark.parametrize("boost", [6.0, 40.0])
-def test_prefill_score_jumps_after_first_tile(boost, nw):
-    """Keys past the first 2 KV tiles are scaled up so later tiles' scores exceed the running max
-    from the first tile by ~20 (boost 6: the speculative single pass keeps P = 2^(s - m_run) up to
-    2^20 in bf16) or by > 64 (boost 40: the row sum passes 2^64 and the tile is redone exactly)."""
+@pytest.mark.parametrize("start", [256, 320], ids=["jump_lo_half", "jump_hi_half"])
+def test_prefill_score_jumps_after_first_tile(boost, nw, start):
+    """Keys past `start` are scaled up so later tiles' scores exceed the running max from the first
+    tile by ~20 (boost 6: the speculative single pass keeps P = 2^(s - m_run) up to 2^20 in bf16) or
+    by > 64 (boost 40: the row sum passes 2^64 and the tile is redone exactly); start = 320 puts
+    the jump in the upper half of a 128-key tile."""
     g = torch.Generator().manual_seed(7)
     lens = [1000, 640]
     T, Hq, Hkv = sum(lens), 16, 4
     q = torch.randn(T, Hq, 128, generator=g).bfloat16()
     k = torch.randn(T, Hkv, 128, generator=g)
-    k[256:1000] *= boost
-    k[1000 + 256:] *= boost
+    k[start:1000] *= boost
+    k[1000 + start:] *= boost
     k = k.bfloat16()
     v = torch.randn(T, Hkv, 128, generator=g).bfloat16()
     cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32)
@@ -216,7 +218,28 @@ def test_prefill_score_jumps_after_first_tile(boost, nw):
     qd, kd, vd = q.to(DEV), k.to(DEV), v.to(DEV)
     out = A.prefill_varlen(qd, kd, vd, cu.to(DEV), max(lens), config=pcfg(ns=2 if nw == 8 else 3, nw=nw))
     assert not torch.isnan(out).any()
-    check(f"prefill score jumps x{boost} w{nw}", out, ref, sdpa_prefill_bf16(qd, kd, vd, cu, True))
+    check(f"prefill score jumps x{boost} w{nw} from {start}", out, ref, sdpa_prefill_bf16(qd, kd, vd, cu, True))
+
+
+@pytest.mark.parametrize("boost", [6.0, 40.0])
+@pytest.mark.parametrize("start", [256, 320], ids=["jump_lo_half", "jump_hi_half"])
+def test_prefill_score_jumps_block_m_128(boost, start):
+    """The same with one q head per CTA (BLOCK_M = 128: S double-buffered, QK two KV steps ahead)."""
+    g = torch.Generator().manual_seed(8)
+    lens = [900, 500]
+    T, Hq, Hkv = sum(lens), 8, 2
+    q = torch.randn(T, Hq, 128, generator=g).bfloat16()
+    k = torch.randn(T, Hkv, 128, generator=g)
+    k[start:900] *= boost
+    k[900 + start:] *= boost
+    k = k.bfloat16()
+    v = torch.randn(T, Hkv, 128, generator=g).bfloat16()
+    cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32)
+    ref = oracle.prefill(q, k, v, cu)
+    qd, kd, vd = q.to(DEV), k.to(DEV), v.to(DEV)
+    out = A.prefill_varlen(qd, kd, vd, cu.to(DEV), max(lens), config=pcfg(bm=128, ns=3))
+    assert not torch.isnan(out).any()
+    check(f"prefill score jumps bm128 x{boost} from {start}", out, ref, sdpa_prefill_bf16(qd, kd, vd, cu, True))
 
 
 @pytest.mark.parametrize("nw", [4, 8])
