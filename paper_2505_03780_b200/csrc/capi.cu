@@ -92,6 +92,27 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// Same with CTA pairs: clusters of 2 along x (the pair lands on one TPC; cta_group::2 kernels)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k_pair(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                          Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ------------------------------------------------------------------ tensor maps
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -198,10 +219,10 @@ bool prefill_speculate() {
   return v == 1;
 }
 
-template <int NQ, int BN, int NS, int SPLIT>
+template <int NQ, int BN, int NS, int SPLIT, bool PAIR = false>
 int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
-  using C = b200::PrefillCfg<NQ, BN, NS, SPLIT>;
-  auto kern = b200::prefill_fwd_kernel<NQ, BN, NS, kPrefillEmu, SPLIT>;
+  using C = b200::PrefillCfg<NQ, BN, NS, SPLIT, PAIR>;
+  auto kern = b200::prefill_fwd_kernel<NQ, BN, NS, kPrefillEmu, SPLIT, PAIR>;
   if (int rc0 = ensure_smem_attr(reinterpret_cast<const void*>(kern), C::SMEM_BYTES,
                                "cudaFuncSetAttribute(prefill)"))
     return rc0;
@@ -211,8 +232,9 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   if ((rc = make_map_3d(&mq, p->q, D, p->num_q_heads, p->total_tokens, D * 2ull, (uint64_t)p->num_q_heads * D * 2,
                         1, C::BM)))
     return rc;
+  // PAIR: each CTA of the pair loads BN/2 keys of a K tile (and 64 d columns of all BN keys of V)
   if ((rc = make_map_3d(&mk, p->k, D, p->num_kv_heads, p->total_tokens, D * 2ull,
-                        (uint64_t)p->num_kv_heads * D * 2, 1, BN)))
+                        (uint64_t)p->num_kv_heads * D * 2, 1, PAIR ? BN / 2 : BN)))
     return rc;
   if ((rc = make_map_3d(&mv, p->v, D, p->num_kv_heads, p->total_tokens, D * 2ull,
                         (uint64_t)p->num_kv_heads * D * 2, 1, BN)))
@@ -244,15 +266,20 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   a.num_q_heads = p->num_q_heads;
   a.group = p->num_q_heads / p->num_kv_heads;
   a.causal = p->causal;
-  a.num_hg = p->num_q_heads / NQ;
+  a.num_hg = p->num_q_heads / (NQ * (PAIR ? 2 : 1));
   a.single_nqb = single ? (p->max_seqlen + C::BM - 1) / C::BM : 0;
   const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / sqrtf((float)p->head_dim);
   a.scale_log2 = scale * 1.4426950408889634f;
   a.speculate = prefill_speculate() ? 1 : 0;
   // persistent: never more CTAs than work items (upper bound without a device read)
   const long long items_ub = ((long long)p->total_tokens / 128 + p->num_seqs) * a.num_hg;
-  const int ctas = (int)std::min<long long>(num_sms(), std::max<long long>(1, items_ub));
-  e = launch_k(kern, dim3(ctas), dim3(C::NTHREADS), C::SMEM_BYTES, stream, mq, mk, mv, a);
+  if constexpr (PAIR) {
+    const int pairs = (int)std::min<long long>(num_sms() / 2, std::max<long long>(1, items_ub));
+    e = launch_k_pair(kern, dim3(2 * pairs), dim3(C::NTHREADS), C::SMEM_BYTES, stream, mq, mk, mv, a);
+  } else {
+    const int ctas = (int)std::min<long long>(num_sms(), std::max<long long>(1, items_ub));
+    e = launch_k(kern, dim3(ctas), dim3(C::NTHREADS), C::SMEM_BYTES, stream, mq, mk, mv, a);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
   return B200ATTN_OK;
 }
@@ -261,6 +288,7 @@ struct PrefillEntry {
   int nq, bn, ns, nw;
   PrefillLauncher fn;
   int smem;
+  int pair;  // waves_per_eu = 2: the item runs on a CTA pair (cta_group::2)
 };
 
 // num_warps = softmax warps per 128-row Q tile: 4 (one thread per S row) or 8 (two threads per
@@ -268,14 +296,20 @@ struct PrefillEntry {
 // num_stages at 2)
 #define PF(NQ, BN, NS, NW)                                                 \
   {NQ, BN, NS, NW, &launch_prefill<NQ, BN, NS, NW / 4>,                    \
-   b200::PrefillCfg<NQ, BN, NS, NW / 4>::SMEM_BYTES}
+   b200::PrefillCfg<NQ, BN, NS, NW / 4>::SMEM_BYTES, 0}
+#define PF2(NQ, NS)                                                        \
+  {NQ, 128, NS, 4, &launch_prefill<NQ, 128, NS, 1, true>,                  \
+   b200::PrefillCfg<NQ, 128, NS, 1, true>::SMEM_BYTES, 1}
 const PrefillEntry kPrefill[] = {
     PF(2, 128, 1, 4), PF(2, 128, 2, 4), PF(2, 128, 3, 4), PF(2, 128, 4, 4), PF(2, 64, 1, 4),  PF(2, 64, 2, 4),
     PF(2, 64, 3, 4),  PF(2, 64, 4, 4),  PF(1, 128, 1, 4), PF(1, 128, 2, 4), PF(1, 128, 3, 4), PF(1, 128, 4, 4),
     PF(1, 64, 1, 4),  PF(1, 64, 2, 4),  PF(1, 64, 3, 4),  PF(1, 64, 4, 4),  PF(2, 128, 1, 8), PF(2, 128, 2, 8),
     PF(1, 128, 1, 8), PF(1, 128, 2, 8),
+    // CTA pairs (waves_per_eu = 2): BLOCK_M = 256 -> 4 q heads per pair, 128 -> 2
+    PF2(2, 1), PF2(2, 2), PF2(2, 3), PF2(1, 1), PF2(1, 2), PF2(1, 3),
 };
 #undef PF
+#undef PF2
 
 int check_prefill(const b200attn_prefill_params* p, const b200attn_prefill_variant* v, const PrefillEntry** out) {
   if (!p || !v) return fail(B200ATTN_BAD_ARGS, "null params/variant");
@@ -293,14 +327,15 @@ int check_prefill(const b200attn_prefill_params* p, const b200attn_prefill_varia
                 v->num_warps);
   if (v->num_warps == 8 && v->block_n != 128)
     return fail(B200ATTN_UNSUPPORTED_CONFIG, "num_warps=8 splits 128-column S rows in halves; BLOCK_N must be 128");
-  if (v->waves_per_eu != 1)
+  if (v->waves_per_eu != 1 && v->waves_per_eu != 2)
     return fail(B200ATTN_UNSUPPORTED_CONFIG,
-                "waves_per_eu=%d: AMD occupancy hint; one attention CTA owns an SM's TMEM on sm_100a",
+                "waves_per_eu=%d: 1 = one CTA per work item, 2 = a CTA pair (cta_group::2) per work item",
                 v->waves_per_eu);
   const int nq = v->block_m / 128;
+  const int pair = v->waves_per_eu == 2 ? 1 : 0;
   const PrefillEntry* e = nullptr;
   for (const auto& x : kPrefill)
-    if (x.nq == nq && x.bn == v->block_n && x.ns == v->num_stages && x.nw == v->num_warps) e = &x;
+    if (x.nq == nq && x.bn == v->block_n && x.ns == v->num_stages && x.nw == v->num_warps && x.pair == pair) e = &x;
   if (!e)
     return fail(B200ATTN_UNSUPPORTED_CONFIG,
                 "no compiled variant for BLOCK_M=%d BLOCK_N=%d num_warps=%d num_stages=%d", v->block_m,
@@ -316,6 +351,10 @@ int check_prefill(const b200attn_prefill_params* p, const b200attn_prefill_varia
   if (nq == 2 && group % 2)
     return fail(B200ATTN_UNSUPPORTED_CONFIG,
                 "BLOCK_M=256 pairs two q heads of one kv head; GQA group %d is odd", group);
+  if (pair && group % (2 * nq))
+    return fail(B200ATTN_UNSUPPORTED_CONFIG,
+                "waves_per_eu=2 runs %d q heads of one kv head on a CTA pair; GQA group %d is not a multiple",
+                2 * nq, group);
   if (p->num_seqs <= 0 || p->num_seqs > 65535 || p->total_tokens < 0 || p->max_seqlen < 0)
     return fail(B200ATTN_BAD_ARGS, "num_seqs=%d total_tokens=%d max_seqlen=%d", p->num_seqs, p->total_tokens,
                 p->max_seqlen);

@@ -55,12 +55,18 @@ struct PrefillKernelArgs {
 // faster layout (a 128-column slice: 1053 cycles on two warps vs 1139 on one,
 // scripts/probes/softmax_probe.cu); inside the kernel the tile softmax did not get shorter, and the
 // sweep picks SPLIT = 2 only for some small shapes (DESIGN.md §4 K1).
-template <int NQ, int BN, int NSTAGE_CFG, int SPLIT = 1>
+// PAIR (waves_per_eu = 2): the work item runs on a CTA pair (2-CTA cluster, cta_group::2).  Each
+// CTA keeps its own NQ Q tiles (heads rank*NQ + t of the item's 2*NQ) and loads HALF of every K
+// tile (keys rank*BN/2 ..) and HALF of every V tile (d columns rank*64 ..); one M = 256 MMA of the
+// leader reads B once for both CTAs' Q tiles, so per CTA a K=16 QK^T step reads 4 KB of Q + 2 KB of
+// K in 64 cycles (96 B/clk) instead of 8 KB (128 B/clk, the shared-memory ceiling).
+template <int NQ, int BN, int NSTAGE_CFG, int SPLIT = 1, bool PAIR = false>
 struct PrefillCfg {
   static constexpr int D = 128;
   static constexpr int BM = 128;
   static constexpr int NCOL = BN / SPLIT;                    // S columns per softmax thread
-  static constexpr int NSLOT = (NSTAGE_CFG + 1) * 128 / BN;  // ring = (num_stages + 1) x 32 KB
+  static constexpr int KV_BYTES = PAIR ? BN * D : BN * D * 2;  // one K or V tile (per CTA)
+  static constexpr int NSLOT = (NSTAGE_CFG + 1) * 32768 / KV_BYTES;  // ring = (num_stages + 1) x 32 KB
   static constexpr int NUM_SOFTMAX_WARPS = 4 * NQ * SPLIT;
   static constexpr int TILE_THREADS = 128 * SPLIT;           // softmax threads per Q tile
   static constexpr int TMA_WARP = NUM_SOFTMAX_WARPS;
@@ -86,9 +92,14 @@ struct PrefillCfg {
                                32 * NUM_SOFTMAX_WARPS * REG_SOFTMAX + 128 * REG_OTHER <= NTHREADS * REG_LAUNCH),
                 "setmaxnreg split exceeds the launch allocation");
   static constexpr int Q_BYTES = BM * D * 2;   // 32 KB per Q tile (2 SW128 halves)
-  static constexpr int KV_BYTES = BN * D * 2;  // one K or V tile
   static constexpr int HALF_Q = BM * 128;
-  static constexpr int HALF_KV = BN * 128;
+  static constexpr int HALF_KV = BN * 128;     // V: offset of the second 64-column d block (unpaired)
+  static constexpr int HALF_K = PAIR ? (BN / 2) * 128 : BN * 128;  // K: offset of the second d half
+  // consumer arrivals on the leader's barriers: its own threads arrive locally, the peer's warps
+  // arrive remotely, one per warp
+  static constexpr int ARRIVE_P = PAIR ? TILE_THREADS + 4 : TILE_THREADS;  // p_full / o_free per tile
+  static constexpr int ARRIVE_ITEM = PAIR ? 2 + TILE_THREADS * NQ + 4 * NQ : 1 + TILE_THREADS * NQ;
+  static_assert(!PAIR || (SPLIT == 1 && BN == 128), "CTA pair: 4 softmax warps per tile, BLOCK_N = 128");
   // Q is double-buffered when the ring leaves room: the next item's Q lands during this item
   // SPLIT = 2: per-row exchange of half-row maxima (by step parity) and half-row sums
   static constexpr int XCH_FLOATS = (SPLIT > 1) ? 3 * NQ * SPLIT * 128 : 0;
@@ -104,7 +115,7 @@ struct PrefillCfg {
   static constexpr int LA = SB;                                       // QK lookahead (KV steps)
   // q_full[2], q_empty[2], kv_full/empty[NSLOT], s_full[NQ][SB], p_full[NQ][2], o_done[NQ][2],
   // o_free[NQ], item_full/empty[2]
-  static constexpr int NUM_BARS = 4 + 2 * NSLOT + NQ * SB + 2 * NQ + 2 * NQ + NQ + 4;
+  static constexpr int NUM_BARS = 4 + 2 * NSLOT + NQ * SB + 2 * NQ + 2 * NQ + NQ + 4 + 1;
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
   static constexpr uint32_t TMEM_COLS = 512;
   __host__ __device__ static constexpr uint32_t S_COL(int t, int b) { return (t * SB + b) * BN; }
@@ -312,11 +323,11 @@ __device__ unsigned long long g_trace[16][512];  // 8..11: P done by warp 0..3 o
   } while (0)
 #endif
 
-template <int NQ, int BN, int NSTAGE_CFG, int EMU, int SPLIT>
-__global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREADS, 1)
+template <int NQ, int BN, int NSTAGE_CFG, int EMU, int SPLIT, bool PAIR = false>
+__global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::NTHREADS, 1)
     prefill_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
                        const __grid_constant__ CUtensorMap tmap_v, const PrefillKernelArgs args) {
-  using C = PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>;
+  using C = PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>;
   constexpr int D = C::D, BM = C::BM, NS = C::NSLOT, NCOL = C::NCOL;
 
   extern __shared__ uint8_t smem_raw[];
@@ -338,6 +349,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
   uint64_t* o_free = o_done + 2 * NQ;      // [NQ]      epilogue of O_t done (128 arrivals)
   uint64_t* item_full = o_free + NQ;       // [2]
   uint64_t* item_empty = item_full + 2;
+  uint64_t* drain = item_empty + 2;         // PAIR: the leader's MMA warp waits its last MMAs out
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS);
 
   const int warp = warp_id();
@@ -354,28 +366,56 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
     }
     for (int t = 0; t < NQ; ++t) {
       for (int b = 0; b < C::SB; ++b) mbar_init(&s_full[t * C::SB + b], 1);
-      mbar_init(&p_full[2 * t], C::TILE_THREADS);
-      mbar_init(&p_full[2 * t + 1], C::TILE_THREADS);
+      mbar_init(&p_full[2 * t], C::ARRIVE_P);
+      mbar_init(&p_full[2 * t + 1], C::ARRIVE_P);
       mbar_init(&o_done[2 * t], 1);
       mbar_init(&o_done[2 * t + 1], 1);
-      mbar_init(&o_free[t], C::TILE_THREADS);
+      mbar_init(&o_free[t], C::ARRIVE_P);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&item_full[i], 1);
-      mbar_init(&item_empty[i], 1 + C::TILE_THREADS * NQ);
+      mbar_init(&item_empty[i], C::ARRIVE_ITEM);
     }
+    mbar_init(drain, 1);
     fence_barrier_init();
   }
-  if (warp == C::MMA_WARP) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == C::MMA_WARP) {
+    if constexpr (PAIR)
+      tmem_alloc_pair(tmem_slot, C::TMEM_COLS);  // same warp id in both CTAs, same columns
+    else
+      tmem_alloc(tmem_slot, C::TMEM_COLS);
+  }
   if (warp == C::TMA_WARP && lane == 0) {
     tma_prefetch_desc(&tmap_q);
     tma_prefetch_desc(&tmap_k);
     tma_prefetch_desc(&tmap_v);
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync_all();  // barrier inits of both CTAs visible before any remote arrive
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PAIR: cluster rank (0 = leader: scheduler, MMA issuer, owner of the shared barriers);
+  // `lead` maps one of this CTA's barriers to the leader's copy (shared::cluster address)
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  auto lead = [](uint64_t* b) { return mapa_shared(smem_u32(b), 0); };
+  // one arrival per thread on the local barrier (the leader's own), one per warp from the peer
+  auto arrive_consumer = [&](uint64_t* b) {
+    if (PAIR && rank != 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(lead(b));
+    } else {
+      mbar_arrive(b);
+    }
+  };
+  auto wait_cl = [](uint64_t* b, uint32_t par) {  // waits on barriers the peer also arrives on
+    if constexpr (PAIR)
+      mbar_wait_cluster(b, par);
+    else
+      mbar_wait_producer(b, par);
+  };
   griddep_wait();    // PDL: the prologue above overlapped the previous kernel; data access starts here
   griddep_launch();
   // register hand-over (REG_SPLIT): each role adjusts its own limit at the top of its branch, so
@@ -396,45 +436,82 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
       const int total_work = (args.single_nqb > 0 ? args.single_nqb : args.sched[1]) * args.num_hg;
       const uint64_t keep = policy_evict_last();  // K/V tiles are re-read by other q blocks / heads
       int ri = 0;
+      const uint64_t once = policy_evict_first();  // Q tiles are read by one item only
       for (int k = 0;; ++k) {
-        if (k >= 2) mbar_wait_producer(&item_empty[k & 1], ((k >> 1) - 1) & 1);
-        int w = atomicAdd(args.sched, 1);
-        if (w >= total_work) w = -1;
-        item_box[k & 1] = w;
-        mbar_arrive(&item_full[k & 1]);
+        int w;
+        if (!PAIR || rank == 0) {
+          if (k >= 2) wait_cl(&item_empty[k & 1], ((k >> 1) - 1) & 1);
+          w = atomicAdd(args.sched, 1);
+          if (w >= total_work) w = -1;
+          item_box[k & 1] = w;
+          if constexpr (PAIR) {  // the peer's mailbox, then its item_full (release orders the store)
+            st_cluster_u32(mapa_shared(smem_u32((const void*)&item_box[k & 1]), 1), static_cast<uint32_t>(w));
+            mbar_arrive_cluster(mapa_shared(smem_u32(&item_full[k & 1]), 1));
+          }
+          mbar_arrive(&item_full[k & 1]);
+        } else {
+          mbar_wait_cluster(&item_full[k & 1], (k >> 1) & 1);
+          w = item_box[k & 1];
+          mbar_arrive_cluster(lead(&item_empty[k & 1]));
+        }
         if (w < 0) break;
         int seq, qblk, hg;
         prefill_decode_item(w, args, seq, qblk, hg);
         const int seq_start = args.cu_seqlens[seq];
         const int seq_len = args.cu_seqlens[seq + 1] - seq_start;
-        const int h0 = hg * NQ, kvh = h0 / args.group;
+        const int h0 = hg * NQ * (PAIR ? 2 : 1) + static_cast<int>(rank) * NQ, kvh = h0 / args.group;
         const int n_kv = n_kv_of(seq_len, qblk);
         const int qb = (C::QBUF == 2) ? (k & 1) : 0;
         const uint32_t qph = (C::QBUF == 2) ? ((k >> 1) & 1) : (k & 1);
         mbar_wait_producer(&q_empty[qb], qph ^ 1);
-        mbar_arrive_expect_tx(&q_full[qb], NQ * C::Q_BYTES);
-        for (int t = 0; t < NQ; ++t)
-          for (int hf = 0; hf < 2; ++hf)
-            tma_load_3d(sQ + (qb * NQ + t) * C::Q_BYTES + hf * C::HALF_Q, &tmap_q, &q_full[qb], hf * 64, h0 + t,
-                        seq_start + qblk * BM);
+        if constexpr (PAIR) {
+          // both CTAs' bytes complete on the leader's barrier; only the leader arms it (a peer
+          // transfer landing first leaves the tx-count transiently negative, which is allowed)
+          if (rank == 0) mbar_arrive_expect_tx(&q_full[qb], 2 * NQ * C::Q_BYTES);
+          const uint32_t fb = lead(&q_full[qb]);
+          for (int t = 0; t < NQ; ++t)
+            for (int hf = 0; hf < 2; ++hf)
+              tma_load_3d_pair(sQ + (qb * NQ + t) * C::Q_BYTES + hf * C::HALF_Q, &tmap_q, fb, hf * 64, h0 + t,
+                               seq_start + qblk * BM, once);
+        } else {
+          mbar_arrive_expect_tx(&q_full[qb], NQ * C::Q_BYTES);
+          for (int t = 0; t < NQ; ++t)
+            for (int hf = 0; hf < 2; ++hf)
+              tma_load_3d(sQ + (qb * NQ + t) * C::Q_BYTES + hf * C::HALF_Q, &tmap_q, &q_full[qb], hf * 64, h0 + t,
+                          seq_start + qblk * BM);
+        }
         for (int idx = 0; idx < 2 * n_kv; ++idx, ++ri) {
           const int slot = ri % NS;
           mbar_wait_producer(&kv_empty[slot], ((ri / NS) & 1) ^ 1);
-          const CUtensorMap* map = (idx & 1) ? &tmap_v : &tmap_k;
           uint8_t* dst = sKV + slot * C::KV_BYTES;
-          mbar_arrive_expect_tx(&kv_full[slot], C::KV_BYTES);
-          for (int hf = 0; hf < 2; ++hf)
-            tma_load_3d_hint(dst + hf * C::HALF_KV, map, &kv_full[slot], hf * 64, kvh, seq_start + (idx >> 1) * BN,
-                             keep);
+          const int tok0 = seq_start + (idx >> 1) * BN;
+          if constexpr (PAIR) {
+            // K: this CTA's BN/2 keys (both d halves); V: this CTA's 64 d columns of all BN keys
+            if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * C::KV_BYTES);
+            const uint32_t fb = lead(&kv_full[slot]);
+            if ((idx & 1) == 0) {
+              for (int hf = 0; hf < 2; ++hf)
+                tma_load_3d_pair(dst + hf * C::HALF_K, &tmap_k, fb, hf * 64, kvh,
+                                 tok0 + static_cast<int>(rank) * (BN / 2), keep);
+            } else {
+              tma_load_3d_pair(dst, &tmap_v, fb, static_cast<int>(rank) * 64, kvh, tok0, keep);
+            }
+          } else {
+            const CUtensorMap* map = (idx & 1) ? &tmap_v : &tmap_k;
+            mbar_arrive_expect_tx(&kv_full[slot], C::KV_BYTES);
+            for (int hf = 0; hf < 2; ++hf)
+              tma_load_3d_hint(dst + hf * C::HALF_KV, map, &kv_full[slot], hf * 64, kvh, tok0, keep);
+          }
         }
       }
     }
   } else if (warp == C::MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer (whole warp, one elected lane issues)
     regs_other();
-    {
-      constexpr uint32_t IDESC_QK = idesc_bf16_f32(BM, BN, false, false);
-      constexpr uint32_t IDESC_PV = idesc_bf16_f32(BM, D, false, true);
+    if (!PAIR || rank == 0) {  // PAIR: the leader issues the M = 256 MMAs for both CTAs
+      constexpr uint32_t MM = PAIR ? 2 * BM : BM;
+      constexpr uint32_t IDESC_QK = idesc_bf16_f32(MM, BN, false, false);
+      constexpr uint32_t IDESC_PV = idesc_bf16_f32(MM, D, false, true);
       // Descriptors are built once; per-MMA addressing is a 16-B-unit add on the start-address
       // field (smem < 256 KB, so the 14-bit field never carries).  Rebuilding 64-bit descriptors
       // per MMA costs the single issuing thread ~120 cycles and starves the tensor pipe.
@@ -443,14 +520,25 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
       const uint64_t v_desc = sdesc_sw128(smem_u32(sKV), C::HALF_KV, 1024);
       constexpr int SB = C::SB, LA = C::LA;
       int qb = 0;
+      auto commit = [](uint64_t* b) {
+        if constexpr (PAIR)
+          umma_commit_pair_w(b, 3);  // arrives on this barrier in both CTAs
+        else
+          umma_commit_w(b);
+      };
       auto issue_qk = [&](int t, int slot, int buf) {
         const uint64_t qa = q_desc + (((qb * NQ + t) * C::Q_BYTES) >> 4);
         const uint64_t kb = k_desc + ((slot * C::KV_BYTES) >> 4);
-        umma_ss_k128<2, C::HALF_Q / 16, 2, C::HALF_KV / 16>(tmem + C::S_COL(t, buf), qa, kb, IDESC_QK, 0u);
+        if constexpr (PAIR)
+          umma_ss_k128_pair<2, C::HALF_Q / 16, 2, C::HALF_K / 16>(tmem + C::S_COL(t, buf), qa, kb, IDESC_QK, 0u);
+        else
+          umma_ss_k128<2, C::HALF_Q / 16, 2, C::HALF_KV / 16>(tmem + C::S_COL(t, buf), qa, kb, IDESC_QK, 0u);
       };
       auto issue_pv = [&](int t, int slot, int buf, bool acc) {
         const uint64_t vb = v_desc + ((slot * C::KV_BYTES) >> 4);
-        if constexpr (BN == 128) {
+        if constexpr (PAIR) {
+          umma_ts_k128_pair<128, 512>(tmem + C::O_COL(t), tmem + C::S_COL(t, buf), vb, IDESC_PV, acc ? 1u : 0u);
+        } else if constexpr (BN == 128) {
           // SPLIT = 2: P of S columns [64, 128) sits at S column 64 (the second half-row owner's range)
           umma_ts_k128<128, 512, (SPLIT == 2 ? 32 : 0)>(tmem + C::O_COL(t), tmem + C::S_COL(t, buf), vb, IDESC_PV,
                                                        acc ? 1u : 0u);
@@ -474,36 +562,36 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
         const int seq_start = args.cu_seqlens[seq];
         const int n_kv = n_kv_of(args.cu_seqlens[seq + 1] - seq_start, qblk);
         qb = (C::QBUF == 2) ? (k & 1) : 0;
-        mbar_wait_producer(&q_full[qb], (C::QBUF == 2) ? ((k >> 1) & 1) : (k & 1));
+        wait_cl(&q_full[qb], (C::QBUF == 2) ? ((k >> 1) & 1) : (k & 1));
         // QK_t(s) of step s for tile t; per tile, step s uses S buffer (gt + s) % SB
         auto qk_step_tile = [&](int s, int t) {
           const int ki = rbase + 2 * s, kslot = ki % NS;
           if (t == 0) {
-            mbar_wait_producer(&kv_full[kslot], (ki / NS) & 1);
+            wait_cl(&kv_full[kslot], (ki / NS) & 1);
             tc_fence_after();
           }
           const int buf = (gt + s) % SB;
           issue_qk(t, kslot, buf);
-          umma_commit_w(&s_full[t * SB + buf]);
+          commit(&s_full[t * SB + buf]);
           if (t == NQ - 1) {
-            umma_commit_w(&kv_empty[kslot]);
-            if (s == n_kv - 1) umma_commit_w(&q_empty[qb]);
+            commit(&kv_empty[kslot]);
+            if (s == n_kv - 1) commit(&q_empty[qb]);
           }
         };
         for (int s = 0; s < LA && s < n_kv; ++s)
           for (int t = 0; t < NQ; ++t) qk_step_tile(s, t);
         for (int j = 0; j < n_kv; ++j) {
           const int vi = rbase + 2 * j + 1, vslot = vi % NS;
-          mbar_wait_producer(&kv_full[vslot], (vi / NS) & 1);
+          wait_cl(&kv_full[vslot], (vi / NS) & 1);
           TRACE(6, gt + j);
           for (int t = 0; t < NQ; ++t) {
-            mbar_wait_producer(&p_full[2 * t + ((gt + j) & 1)], ((gt + j) >> 1) & 1);
+            wait_cl(&p_full[2 * t + ((gt + j) & 1)], ((gt + j) >> 1) & 1);
             TRACE(4 + t, gt + j);
-            if (j == 0 && k > 0) mbar_wait_producer(&o_free[t], (k - 1) & 1);
+            if (j == 0 && k > 0) wait_cl(&o_free[t], (k - 1) & 1);
             tc_fence_after();
             issue_pv(t, vslot, (gt + j) % SB, j > 0);
-            umma_commit_w(&o_done[2 * t + ((gt + j) & 1)]);
-            if (t == NQ - 1) umma_commit_w(&kv_empty[vslot]);
+            commit(&o_done[2 * t + ((gt + j) & 1)]);
+            if (t == NQ - 1) commit(&kv_empty[vslot]);
             if (j + LA < n_kv) {
               qk_step_tile(j + LA, t);
               if (t == 0) TRACE(7, gt + j);
@@ -512,6 +600,12 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
         }
         rbase += 2 * n_kv;
         gt += n_kv;
+      }
+      if constexpr (PAIR) {
+        // every MMA (and so every multicast arrival into the peer's barriers) has completed before
+        // this warp reaches the teardown's cluster barrier
+        umma_commit_pair_w(drain, 1);
+        mbar_wait(drain, 0);
       }
     }
   } else if (warp < C::NUM_SOFTMAX_WARPS) {
@@ -541,9 +635,12 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
     };
     int gt = 0;
     for (int k = 0;; ++k) {
-      mbar_wait(&item_full[k & 1], (k >> 1) & 1);
+      if (PAIR && rank != 0)
+        mbar_wait_cluster(&item_full[k & 1], (k >> 1) & 1);  // written by the leader
+      else
+        mbar_wait(&item_full[k & 1], (k >> 1) & 1);
       const int w = item_box[k & 1];
-      mbar_arrive(&item_empty[k & 1]);
+      arrive_consumer(&item_empty[k & 1]);
       if (w < 0) break;
       int seq, qblk, hg;
       prefill_decode_item(w, args, seq, qblk, hg);
@@ -579,7 +676,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
           if (row == 0 && hh == 0) TRACE(2 + t, gt + j);
           if (t == 0 && lane == 0 && warp < 4) TRACE(8 + warp, gt + j);
           observe_o_done(gt + j, od_seen);
-          mbar_arrive(&p_full[2 * t + ((gt + j) & 1)]);
+          arrive_consumer(&p_full[2 * t + ((gt + j) & 1)]);
           continue;
         }
         float mt = warp_edge ? softmax_rowmax<NCOL, true>(s_addr, kv0h, lim)
@@ -624,7 +721,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
         if (row == 0 && hh == 0) TRACE(2 + t, gt + j);
         if (t == 0 && lane == 0 && warp < 4) TRACE(8 + warp, gt + j);
         observe_o_done(gt + j, od_seen);
-        mbar_arrive(&p_full[2 * t + ((gt + j) & 1)]);
+        arrive_consumer(&p_full[2 * t + ((gt + j) & 1)]);
       }
 
       // ---------------------------------------------------------- epilogue for this item
@@ -636,7 +733,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
       }
       mbar_wait(&o_done[2 * t + ((gt + n_kv - 1) & 1)], ((gt + n_kv - 1) >> 1) & 1);  // last PV_t
       tc_fence_after();
-      const int h = hg * NQ + t;
+      const int h = hg * NQ * (PAIR ? 2 : 1) + static_cast<int>(rank) * NQ + t;
       const bool valid = q_pos < seq_len;
       const float inv_l = (l_tot > 0.f) ? 1.f / l_tot : 0.f;
       __nv_bfloat16* orow = args.o + (static_cast<size_t>(seq_start + q_pos) * args.num_q_heads + h) * D + hh * OCOLS;
@@ -655,7 +752,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
         }
       }
       tc_fence_before();
-      mbar_arrive(&o_free[t]);
+      arrive_consumer(&o_free[t]);
       if (valid && hh == 0 && args.lse != nullptr) {
         args.lse[static_cast<size_t>(h) * args.total_tokens + seq_start + q_pos] =
             (l_tot > 0.f) ? (m_run + __log2f(l_tot)) * 0.69314718055994530942f : -INFINITY;
@@ -668,10 +765,14 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT>::NTHREAD
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // no remote arrive / MMA into the other CTA is in flight
   if (warp == C::MMA_WARP) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem, C::TMEM_COLS);
+    if constexpr (PAIR)
+      tmem_dealloc_pair(tmem, C::TMEM_COLS);
+    else
+      tmem_dealloc(tmem, C::TMEM_COLS);
   }
   if (threadIdx.x == 0) {
     // every CTA has drawn its final (out-of-range) item before getting here: the last one out

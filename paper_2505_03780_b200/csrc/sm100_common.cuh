@@ -332,6 +332,137 @@ __device__ __forceinline__ void umma_ts_k128(uint32_t d, uint32_t a_tmem, uint64
       : "memory");
 }
 
+// ------------------------------------------------ CTA pair (cta_group::2, a 2-CTA cluster on one TPC)
+// One elected thread of the leader CTA (cluster rank 0) issues an M = 256 MMA: rows 0..127 of A
+// come from the leader's shared memory (or TMEM), rows 128..255 from the peer's at the same
+// offset; B is split along N across the pair (each CTA holds N/2 rows of it at the same offset);
+// each CTA's TMEM receives its own 128 rows of D at the same TMEM address.
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cta address of this CTA -> shared::cluster address of the same offset in CTA `rank`
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+// wait with cluster-scope acquire: arrivals came from the peer CTA (release.cluster) or its TMA
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t spins = 0;
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (++spins == B200_WAIT_TRAP_SPINS) __trap();
+  }
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load into this CTA's shared memory whose completion is counted on an mbarrier of either CTA
+// of the pair (`bar_cluster` from mapa_shared): both CTAs' halves land on the leader's barrier.
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1, int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// commit of the pair's MMAs, arriving on the barrier at this offset in both CTAs
+__device__ __forceinline__ void umma_commit_pair_w(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::
+          "r"(smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
+}
+// cta_group::2 versions (issued by the leader CTA of a pair; same operand stepping)
+template <int AS, int AH, int BS, int BH>
+__device__ __forceinline__ void umma_ss_k128_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred e, p;\n\t.reg .b64 ta, tb;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "setp.eq.u32 p, 0, 0;\n\t"
+      "add.s64 ta, %1, %5;\n\tadd.s64 tb, %2, %6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %7;\n\tadd.s64 tb, %2, %8;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %9;\n\tadd.s64 tb, %2, %10;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %11;\n\tadd.s64 tb, %2, %12;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %13;\n\tadd.s64 tb, %2, %14;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %15;\n\tadd.s64 tb, %2, %16;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "add.s64 ta, %1, %17;\n\tadd.s64 tb, %2, %18;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], ta, tb, %3, p;\n\t"
+      "}"
+      :: "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc), "n"(((1 & 3) * AS + (1 >> 2) * AH)), "n"(((1 & 3) * BS + (1 >> 2) * BH)),
+         "n"(((2 & 3) * AS + (2 >> 2) * AH)), "n"(((2 & 3) * BS + (2 >> 2) * BH)),
+         "n"(((3 & 3) * AS + (3 >> 2) * AH)), "n"(((3 & 3) * BS + (3 >> 2) * BH)),
+         "n"(((4 & 3) * AS + (4 >> 2) * AH)), "n"(((4 & 3) * BS + (4 >> 2) * BH)),
+         "n"(((5 & 3) * AS + (5 >> 2) * AH)), "n"(((5 & 3) * BS + (5 >> 2) * BH)),
+         "n"(((6 & 3) * AS + (6 >> 2) * AH)), "n"(((6 & 3) * BS + (6 >> 2) * BH)),
+         "n"(((7 & 3) * AS + (7 >> 2) * AH)), "n"(((7 & 3) * BS + (7 >> 2) * BH))
+      : "memory");
+}
+
+template <int BS, int BH, int AGAP = 0>
+__device__ __forceinline__ void umma_ts_k128_pair(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred e, p;\n\t.reg .b32 ta;\n\t.reg .b64 tb;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "setp.eq.u32 p, 0, 0;\n\t"
+      "add.s32 ta, %1, 8;\n\tadd.s64 tb, %2, %5;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "add.s32 ta, %1, 16;\n\tadd.s64 tb, %2, %6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "add.s32 ta, %1, 24;\n\tadd.s64 tb, %2, %7;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "add.s32 ta, %1, %12;\n\tadd.s64 tb, %2, %8;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "add.s32 ta, %1, %13;\n\tadd.s64 tb, %2, %9;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "add.s32 ta, %1, %14;\n\tadd.s64 tb, %2, %10;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "add.s32 ta, %1, %15;\n\tadd.s64 tb, %2, %11;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], tb, %3, p;\n\t"
+      "}"
+      :: "r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "n"(((1 & 3) * BS + (1 >> 2) * BH)), "n"(((2 & 3) * BS + (2 >> 2) * BH)), "n"(((3 & 3) * BS + (3 >> 2) * BH)), "n"(((4 & 3) * BS + (4 >> 2) * BH)), "n"(((5 & 3) * BS + (5 >> 2) * BH)), "n"(((6 & 3) * BS + (6 >> 2) * BH)), "n"(((7 & 3) * BS + (7 >> 2) * BH)),
+         "n"(32 + AGAP), "n"(40 + AGAP), "n"(48 + AGAP), "n"(56 + AGAP)
+      : "memory");
+}
+
 // Arrive on an mbarrier once every previously issued tcgen05 op of this thread completes.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

@@ -61,12 +61,26 @@ def test_prefill_supported_accepts_compiled_variants():
     (dict(num_warps=2), _native.UNSUPPORTED_CONFIG),
     (dict(num_warps=8, num_stages=3), _native.UNSUPPORTED_CONFIG),
     (dict(num_warps=8, num_stages=2, BLOCK_N=64), _native.UNSUPPORTED_CONFIG),
-    (dict(waves_per_eu=2), _native.UNSUPPORTED_CONFIG),
+    (dict(waves_per_eu=2, num_stages=4), _native.UNSUPPORTED_CONFIG),
+    (dict(waves_per_eu=2, BLOCK_N=64), _native.UNSUPPORTED_CONFIG),
+    (dict(waves_per_eu=2, num_warps=8, num_stages=2), _native.UNSUPPORTED_CONFIG),
     (dict(num_stages=5), _native.UNSUPPORTED_CONFIG),
 ])
 def test_prefill_rejections(kw, code):
     rc, why = A.prefill_supported(config=cfg(**kw), **C1)
     assert rc == code and why
+
+
+def test_prefill_cta_pair_variants():
+    """waves_per_eu = 2: the work item on a CTA pair; BLOCK_M = 256 needs 4 q heads per kv head."""
+    for bm in (128, 256):
+        for ns in (1, 2, 3):
+            rc, why = A.prefill_supported(config=cfg(BLOCK_M=bm, num_stages=ns, waves_per_eu=2), **C1)
+            assert rc == _native.OK, why
+    rc, why = A.prefill_supported((100, 8, 128), 4, 1, 100, cfg(BLOCK_M=256, waves_per_eu=2))
+    assert rc == _native.UNSUPPORTED_CONFIG and "multiple" in why  # group 2
+    rc, _ = A.prefill_supported((100, 8, 128), 4, 1, 100, cfg(BLOCK_M=128, waves_per_eu=2))
+    assert rc == _native.OK
 
 
 def test_prefill_head_pair_needs_even_group():
@@ -87,8 +101,9 @@ def test_flash_attention_space_variant_map():
         if rc != _native.OK:
             assert why
     # num_warps 4: BLOCK_M {128,256} x BLOCK_N {64,128} x num_stages 1..4 (x PRE_LOAD_V, which needs
-    # stages <= 2) = 24; num_warps 8: BLOCK_M {128,256} x BLOCK_N 128 x num_stages {1,2} x PRE_LOAD_V = 8
-    assert ok == 32
+    # stages <= 2) = 24; num_warps 8: BLOCK_M {128,256} x BLOCK_N 128 x num_stages {1,2} x PRE_LOAD_V = 8;
+    # CTA pairs (waves_per_eu 2): BLOCK_M {128,256} x BLOCK_N 128 x num_stages 1..3 x PRE_LOAD_V = 10
+    assert ok == 42
 
 
 def test_decode_supported_and_splits():
