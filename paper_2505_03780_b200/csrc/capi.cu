@@ -206,7 +206,22 @@ size_t prefill_ws_ints(const b200attn_prefill_params* p, int* nkeys_out) {
   const int nkeys = (p->max_seqlen + 127) / 128;
   const size_t pairs = (size_t)p->total_tokens / 128 + (size_t)p->num_seqs + 1;
   if (nkeys_out) *nkeys_out = nkeys;
-  return 3 + (size_t)nkeys + pairs;
+  // items: one int per (seq, q block) pair, or two per (seq, q block, kv head) entry when banded
+  return 3 + (size_t)nkeys + 2 * pairs * (size_t)std::max(1, p->num_kv_heads);
+}
+
+// L2-aware banded item order (PrefillKernelArgs::band): on when the K/V the CTAs stream exceeds
+// ~half of the 126-MB L2, off below (pure longest-first balances small problems best).
+// B200ATTN_PREFILL_BAND=<n> forces a band of n q blocks (0 = off) for A/B.
+int prefill_band(const b200attn_prefill_params* p) {
+  static int forced = -2;
+  if (forced == -2) {
+    const char* e = getenv("B200ATTN_PREFILL_BAND");
+    forced = e ? atoi(e) : -1;
+  }
+  if (forced >= 0) return forced;
+  const double kv_bytes = (double)p->total_tokens * p->num_kv_heads * p->head_dim * 2.0 * 2.0;
+  return kv_bytes > 64.0 * 1024 * 1024 ? 32 : 0;
 }
 
 // Single-pass speculative softmax on interior tiles (default); B200ATTN_PREFILL_SPECULATE=0 -> two-pass
@@ -245,8 +260,14 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   // one sequence: its q blocks in reverse are already longest-first, so no schedule kernel; the
   // kernel's last CTA re-zeroes the work counter (the workspace starts zeroed, see header)
   const bool single = (p->num_seqs == 1);
+  const int band = prefill_band(p);
   cudaError_t e;
-  if (!single) {
+  if (!single && band > 0) {
+    const int nbands = (nkeys + band - 1) / band;
+    e = launch_k(b200::prefill_schedule_banded_kernel, dim3(1), dim3(1024), 0, stream, p->cu_seqlens, p->num_seqs,
+                 p->causal, p->num_kv_heads, band, nbands, 3 + nkeys, ws);
+    if (e != cudaSuccess) return cuda_fail(e, "prefill schedule launch");
+  } else if (!single) {
     const size_t hist_bytes = (size_t)nkeys * sizeof(int32_t);
     if (hist_bytes <= 40 * 1024)
       e = launch_k(b200::prefill_schedule_kernel<true>, dim3(1), dim3(1024), hist_bytes, stream, p->cu_seqlens,
@@ -271,6 +292,8 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / sqrtf((float)p->head_dim);
   a.scale_log2 = scale * 1.4426950408889634f;
   a.speculate = prefill_speculate() ? 1 : 0;
+  a.band = band;
+  a.hpk = a.num_hg / p->num_kv_heads;
   // persistent: never more CTAs than work items (upper bound without a device read)
   const long long items_ub = ((long long)p->total_tokens / 128 + p->num_seqs) * a.num_hg;
   if constexpr (PAIR) {

@@ -48,6 +48,13 @@ struct PrefillKernelArgs {
                        // q blocks longest first; the work counter is then reset by the last CTA
   float scale_log2;  // softmax_scale * log2(e)
   int32_t speculate;  // 1: interior tiles take the single-pass path against the running max
+  // L2-aware order (band > 0; problems whose K/V exceeds ~half of L2): q blocks are taken in bands
+  // of `band` blocks, longest band first; inside a band by (sequence, kv head), q block descending,
+  // so the CTAs in flight share a few (sequence, kv head) K/V streams instead of all of them.
+  // items then holds 2 ints per entry: (seq << 16) | q block, kv head; an entry expands to `hpk`
+  // work items (the head groups of that kv head).
+  int32_t band;
+  int32_t hpk;  // head groups per kv head (num_hg / Hkv)
 };
 
 // SPLIT = softmax warps per TMEM lane quadrant (num_warps / 4): with SPLIT = 2 two threads share
@@ -168,6 +175,28 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float& y0, float&
 
 __device__ __forceinline__ void prefill_decode_item(int w, const PrefillKernelArgs& a, int& seq, int& qblk,
                                                     int& hg) {
+  if (a.band > 0) {
+    if (a.single_nqb > 0) {  // bands from the top q block down; all but the last are full
+      const int per_band = a.band * a.num_hg;
+      const int i = w / per_band;
+      const int r = w - i * per_band;
+      const int nq = min(a.band, a.single_nqb - i * a.band);
+      const int per_kvh = nq * a.hpk;
+      const int kvh = r / per_kvh;
+      const int r2 = r - kvh * per_kvh;
+      const int e = r2 / a.hpk;
+      seq = 0;
+      qblk = a.single_nqb - 1 - i * a.band - e;
+      hg = kvh * a.hpk + (r2 - e * a.hpk);
+    } else {
+      const int e = w / a.hpk;
+      const uint32_t it = static_cast<uint32_t>(a.items[2 * e]);
+      seq = static_cast<int>(it >> 16);
+      qblk = static_cast<int>(it & 0xFFFFu);
+      hg = a.items[2 * e + 1] * a.hpk + (w - e * a.hpk);
+    }
+    return;
+  }
   const int pair = w / a.num_hg;
   hg = w - pair * a.num_hg;
   if (a.single_nqb > 0) {
@@ -855,6 +884,82 @@ __global__ void __launch_bounds__(1024) prefill_schedule_kernel(const int32_t* _
   if (tid == 0) {
     ws[0] = 0;
     ws[1] = part[1023];
+  }
+}
+
+// L2-aware banded work list (band > 0, see PrefillKernelArgs): bands of `band` q blocks from the
+// top band down (causal; non-causal: a sequence's items all sit in the band of its block count),
+// inside a band by sequence, kv head, q block descending.  One CTA: per band a block-wide scan of
+// the per-sequence entry counts, then each thread writes its sequences' entries.  Used only for
+// problems whose K/V exceeds ~half of L2, where the prefill runs for >= ~0.5 ms.
+// ws: [0] work counter, [1] n_pairs, [2] done counter, entries (2 ints each) at ws + items_off.
+__global__ void __launch_bounds__(1024) prefill_schedule_banded_kernel(const int32_t* __restrict__ cu, int num_seqs,
+                                                                       int causal, int hkv, int band, int nbands,
+                                                                       int items_off, int32_t* __restrict__ ws) {
+  int32_t* ent = ws + items_off;
+  __shared__ int32_t part[1024];
+  const int tid = threadIdx.x;
+  griddep_wait();
+  griddep_launch();
+  const int per = (num_seqs + 1023) / 1024;
+  const int s0 = tid * per;
+  auto nqb_of = [&](int s) { return (cu[s + 1] - cu[s] + 127) / 128; };
+  auto range = [&](int k, int nqb, int& lo, int& hi) {  // q blocks of band k: [lo, hi)
+    if (causal) {
+      lo = k * band;
+      hi = min(nqb, lo + band);
+    } else {
+      const bool mine = nqb > 0 && (nqb - 1) / band == k;
+      lo = 0;
+      hi = mine ? nqb : 0;
+    }
+  };
+  int pairs_local = 0;
+  for (int i = 0; i < per; ++i)
+    if (s0 + i < num_seqs) pairs_local += nqb_of(s0 + i);
+  int base = 0;
+  for (int k = nbands - 1; k >= 0; --k) {
+    int local = 0;
+    for (int i = 0; i < per; ++i) {
+      const int s = s0 + i;
+      if (s >= num_seqs) break;
+      int lo, hi;
+      range(k, nqb_of(s), lo, hi);
+      local += max(0, hi - lo) * hkv;
+    }
+    part[tid] = local;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      const int v = tid >= off ? part[tid - off] : 0;
+      __syncthreads();
+      part[tid] += v;
+      __syncthreads();
+    }
+    int o = base + part[tid] - local;
+    for (int i = 0; i < per; ++i) {
+      const int s = s0 + i;
+      if (s >= num_seqs) break;
+      int lo, hi;
+      range(k, nqb_of(s), lo, hi);
+      for (int kvh = 0; kvh < hkv; ++kvh)
+        for (int qb = hi - 1; qb >= lo; --qb, ++o) {
+          ent[2 * o] = static_cast<int32_t>((static_cast<uint32_t>(s) << 16) | static_cast<uint32_t>(qb));
+          ent[2 * o + 1] = kvh;
+        }
+    }
+    base += part[1023];
+    __syncthreads();  // part is rewritten by the next band
+  }
+  // n_pairs = sum of q blocks (block reduction through part)
+  part[tid] = pairs_local;
+  __syncthreads();
+  for (int off = 512; off > 0; off >>= 1) {
+    if (tid < off) part[tid] += part[tid + off];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    ws[0] = 0;
+    ws[1] = part[0];
   }
 }
 

@@ -817,3 +817,56 @@ def test_decode_flat_fused_merge_option(tmp_path):
     ki = torch.tensor(sub, device=DEV)
     check("decode flat fused in-kernel merge", res["out"][sub], ref,
           sdpa_decode_bf16(args[0][ki], args[1], args[2], args[3][ki], args[4][ki]))
+
+
+@pytest.mark.parametrize("band", [1, 2, 3])
+def test_prefill_banded_order_forced(tmp_path, band):
+    """The L2-aware banded work order (on by default only above ~64 MB of K/V) forced onto small
+    problems with tiny bands (B200ATTN_PREFILL_BAND, read once per process -> a subprocess): varlen
+    (schedule kernel) and single-sequence (analytic) item decoding, causal and not, GQA 4 and 8,
+    BLOCK_M 128/256 and the CTA pair; every case vs the oracle."""
+    cases = [([300, 77, 1000, 129, 1], 32, 8, True, pcfg()), ([1000], 32, 8, True, pcfg()),
+             ([700, 129], 16, 2, True, pcfg(128, 128, 2)), ([900], 16, 2, False, pcfg(128, 128, 3)),
+             ([500, 1, 640], 32, 8, False, pcfg()), ([1000, 260], 32, 4, True, pcfg(256, 128, 2, pair=True)),
+             ([1100], 32, 4, True, pcfg(256, 128, 2, pair=True))]
+    script = tmp_path / "banded.py"
+    script.write_text(
+        "import sys, json, torch, numpy as np\n"
+        f"sys.path.insert(0, {str(ROOT)!r})\n"
+        "from paper_2505_03780_b200 import attention as A\n"
+        f"cases = json.loads({json.dumps(json.dumps(cases))})\n"
+        "outs = []\n"
+        "for i, (lens, hq, hkv, causal, cfg) in enumerate(cases):\n"
+        "    g = torch.Generator().manual_seed(100 + i)\n"
+        "    T = sum(lens)\n"
+        "    q, k, v = (torch.randn(T, h, 128, generator=g).bfloat16().cuda() for h in (hq, hkv, hkv))\n"
+        "    cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32).cuda()\n"
+        "    outs.append(A.prefill_varlen(q, k, v, cu, max(lens), causal=causal, config=cfg).cpu())\n"
+        f"torch.save(outs, {str(tmp_path / 'out.pt')!r})\n")
+    env = dict(os.environ, B200ATTN_PREFILL_BAND=str(band))
+    r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    outs = torch.load(tmp_path / "out.pt")
+    for i, (lens, hq, hkv, causal, cfg) in enumerate(cases):
+        g = torch.Generator().manual_seed(100 + i)
+        T = sum(lens)
+        q, k, v = (torch.randn(T, h, 128, generator=g).bfloat16() for h in (hq, hkv, hkv))
+        cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32)
+        ref = oracle.prefill(q, k, v, cu, causal=causal)
+        base = sdpa_prefill_bf16(q.to(DEV), k.to(DEV), v.to(DEV), cu, causal)
+        check(f"prefill banded order band={band} {lens} {hq}/{hkv} causal={causal}"
+              f"{' pair' if cfg['waves_per_eu'] == 2 else ''}", outs[i], ref, base)
+
+
+def test_prefill_1x16k_banded_default():
+    """One 16k-token sequence (K/V 67 MB: the banded order is on by default): every q head of 4
+    spread q blocks vs the oracle (rows are independent)."""
+    x = W.make_prefill(dict(W.C1, seq_len=16384), device="cpu")
+    qd, kd, vd, cud = x.q.to(DEV), x.k.to(DEV), x.v.to(DEV), x.cu_seqlens.to(DEV)
+    out = A.prefill_varlen(qd, kd, vd, cud, x.max_seqlen).cpu()
+    for a in (0, 5000, 12000, 16384 - 32):  # causal: rows up to a+31 see keys [0, a+32)
+        sl = slice(0, a + 32)
+        cu = torch.tensor([0, a + 32], dtype=torch.int32)
+        ref = oracle.prefill_blas(x.q[sl], x.k[sl], x.v[sl], cu)
+        base = sdpa_prefill_bf16(qd[sl], kd[sl], vd[sl], cu, True)
+        check(f"1x16k banded rows {a}..{a + 31}", out[a:a + 32], ref[a:a + 32], base[a:a + 32])
