@@ -70,6 +70,17 @@ for r in "$@"; do
               --shapes C3,1x16k,4x8k,16x8k,1x32k,16x2k --tag band$b; done > ${O}_bandab.log 2>&1; cat ${O}_bandab.log ;;
     bandtests) timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "banded or c3_full or every_compiled" \
              > ${O}_bandtests.log 2>&1; tail -15 ${O}_bandtests.log ;;
+    smalldec) for c in "" '{"TILE_N": 16, "num_splits": 0, "num_stages": 4}'; do
+              timeout 300 python scripts/perf.py time --op decode --shapes d1x128,d1x512,d1x2k,d1x8k,d4x512,d4x2k,d16x512,d16x2k,d64x512,C2 \
+                ${c:+--cfg "$c"} --tag "cfg=${c:-dispatch}"; done > ${O}_smalldec.log 2>&1
+            B200ATTN_LIB=$PWD/paper_2505_03780_b200/_lib/libb200attn_trace.so timeout 300 python scripts/perf.py dtrace \
+              --shapes d16x512,d4x2k,d1x8k,d64x512 --cfg '{"TILE_N": 16, "num_splits": 0, "num_stages": 4}' >> ${O}_smalldec.log 2>&1
+            cat ${O}_smalldec.log ;;
+    mergesmall) S=d1x512,d1x2k,d1x8k,d4x512,d4x2k,d16x512,d64x512,C2; C='{"TILE_N": 16, "num_splits": 0, "num_stages": 4}'
+            { timeout 300 python scripts/perf.py time --op decode --shapes $S --cfg "$C" --partial --tag K2only
+              for v in "B200ATTN_FLAT_MERGE=0" "B200ATTN_FLAT_MERGE=1" "B200ATTN_FLAT_MERGE=0 B200ATTN_PDL_COMBINE=1" "B200ATTN_PDL=0"; do
+                env $v timeout 300 python scripts/perf.py time --op decode --shapes $S --cfg "$C" --tag "$v"; done; } > ${O}_mergesmall.log 2>&1
+            cat ${O}_mergesmall.log ;;
     pairtests) timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "pair or every_compiled" \
              > ${O}_pairtests.log 2>&1; tail -15 ${O}_pairtests.log ;;
     pairab) for c in '{"BLOCK_M": 256, "BLOCK_N": 128, "num_warps": 4, "num_stages": 3, "waves_per_eu": 1, "PRE_LOAD_V": false}' \

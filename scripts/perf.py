@@ -47,6 +47,8 @@ SHAPES = {
     "d1x8k": ("decode", dict(W.C2, batch_size=1, seq_len=8192)), "d16x512": ("decode", dict(W.C2, batch_size=16, seq_len=512)),
     "d4x2k": ("decode", dict(W.C2, batch_size=4, seq_len=2048)), "d1x512": ("decode", dict(W.C2, batch_size=1, seq_len=512)),
     "d64x512": ("decode", dict(W.C2, batch_size=64, seq_len=512)),
+    "d1x2k": ("decode", dict(W.C2, batch_size=1, seq_len=2048)), "d4x512": ("decode", dict(W.C2, batch_size=4, seq_len=512)),
+    "d16x2k": ("decode", dict(W.C2, batch_size=16, seq_len=2048)), "d1x128": ("decode", dict(W.C2, batch_size=1, seq_len=128)),
 }
 
 
@@ -194,12 +196,14 @@ def cmd_dtrace(a):
         for _ in range(5):
             p.run()
         torch.cuda.synchronize()
-        buf = (ctypes.c_ulonglong * (1024 * 8))()
-        lib.b200attn_debug_dtrace(buf, 1024 * 8)
-        t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8).astype(np.int64)
+        buf = (ctypes.c_ulonglong * (1024 * 9))()
+        lib.b200attn_debug_dtrace(buf, 1024 * 9)
+        t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 9).astype(np.int64)
         n = int(p.num_splits) if p.config.get("TILE_N") == 16 else 0
         t = t[:n] if n else t[:148]
-        t0 = t[:, 0].min()
+        smid = t[:, 8].copy()
+        t = t[:, :8]
+        t0 = t[:, 0][t[:, 0] > 0].min()
         rel = (t - t0) / 1e3  # us
         out = {"tag": a.tag, "shape": name, "cfg": p.config, "ctas": int(len(t))}
         for k, nm in enumerate(names):
@@ -207,6 +211,8 @@ def cmd_dtrace(a):
             col = col[(t[:, k] > 0)]
             if len(col):
                 out[nm] = [round(float(col.min()), 2), round(float(np.median(col)), 2), round(float(col.max()), 2)]
+        if a.per_cta:  # per CTA: sm id, first S and last P (us from the earliest entry)
+            out["per_cta"] = [[int(smid[i]), round(float(rel[i, 2]), 2), round(float(rel[i, 3]), 2)] for i in range(len(t))]
         print(json.dumps(out), flush=True)
 
 
@@ -266,6 +272,7 @@ def main():
     ap.add_argument("--partial", action="store_true", help="decode: time K2 / K2' alone (no combine)")
     ap.add_argument("--n", type=int, default=3)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--per-cta", action="store_true", help="dtrace: per-CTA sm id / first S / last P")
     a = ap.parse_args()
     {"time": cmd_time, "single": cmd_single, "prof": cmd_prof, "trace": cmd_trace, "umma-rate": cmd_umma_rate, "e2e": cmd_e2e, "dtrace": cmd_dtrace}[a.cmd](a)
 
