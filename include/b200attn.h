@@ -63,7 +63,7 @@ typedef struct {
   const void* q;              /* [total_tokens, num_q_heads, head_dim] bf16  */
   const void* k;              /* [total_tokens, num_kv_heads, head_dim] bf16 */
   const void* v;              /* [total_tokens, num_kv_heads, head_dim] bf16 */
-  void* o;                    /* [total_tokens, num_q_heads, head_dim] bf16  */
+  void* o;                    /* [total_tokens, num_q_heads, head_dim] bf16, 32-byte aligned */
   const int32_t* cu_seqlens;  /* [num_seqs + 1], device                      */
   float* lse;                 /* optional [num_q_heads, total_tokens] fp32 natural-log LSE, may be NULL */
   int32_t num_seqs;

@@ -382,6 +382,8 @@ int check_prefill(const b200attn_prefill_params* p, const b200attn_prefill_varia
     return fail(B200ATTN_BAD_ARGS, "num_seqs=%d total_tokens=%d max_seqlen=%d", p->num_seqs, p->total_tokens,
                 p->max_seqlen);
   if ((p->max_seqlen + 127) / 128 > 65535) return fail(B200ATTN_BAD_ARGS, "max_seqlen too large");
+  if (reinterpret_cast<uintptr_t>(p->o) % 32)
+    return fail(B200ATTN_BAD_ARGS, "o must be 32-byte aligned (the epilogue writes 32-byte row segments)");
   *out = e;
   return B200ATTN_OK;
 }
@@ -916,6 +918,11 @@ int b200attn_cache_append_fp8(const void* new_k, const void* new_v, void* k_cach
 #ifdef B200_TRACE
 int b200attn_debug_trace(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, b200::g_trace, sizeof(unsigned long long) * (size_t)n);
+}
+int b200attn_debug_ptrace(unsigned long long* host, int n, unsigned* launches) {  // K1 [2][1024][8]
+  int rc = (int)cudaMemcpyFromSymbol(host, b200::g_ptrace, sizeof(unsigned long long) * (size_t)n);
+  if (!rc && launches) rc = (int)cudaMemcpyFromSymbol(launches, b200::g_plaunch, sizeof(unsigned));
+  return rc;
 }
 int b200attn_debug_dtrace(unsigned long long* host, int n) {  // K2' per-CTA timeline [1024][8]
   return (int)cudaMemcpyFromSymbol(host, b200::g_dtrace, sizeof(unsigned long long) * (size_t)n);

@@ -341,12 +341,36 @@ __device__ __forceinline__ bool softmax_speculative(uint32_t s_addr, float sl2, 
 
 #ifdef B200_TRACE
 // debug-only event trace of CTA 0: [event][slot] clock64 stamps
-__device__ unsigned long long g_trace[16][512];  // 8..11: P done by warp 0..3 of tile 0; 12..15: S seen
+// event 16: one-off stamps of CTA 0's first item — 0 entry, 1 barriers + TMEM ready, 2 past
+// griddepcontrol.wait, 3 MMA warp saw Q, 4 first S seen by row 0, 5 epilogue start, 6 epilogue
+// done, 7 exit
+__device__ unsigned long long g_trace[17][512];  // 8..11: P done by warp 0..3 of tile 0; 12..15: S seen
 #define TRACE(ev, slot)                                                        \
   do {                                                                        \
     if (blockIdx.x == 0 && (slot) < 512) g_trace[ev][slot] = clock64();        \
   } while (0)
+// per-CTA %globaltimer stamps of the last two launches (by launch parity): 0 entry, 1 past
+// griddepcontrol.wait, 2 work done, 3 exit; g_plaunch counts launches (bumped by the last CTA out)
+__device__ unsigned long long g_ptrace[2][1024][8];  // [4], [5]: clock64 at entry / exit (SM clock);
+                                                     // [6]: first item, [7]: its epilogue done
+__device__ unsigned int g_plaunch;
+__device__ __forceinline__ void ptrace(unsigned par, int ev) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (blockIdx.x < 1024) {
+    g_ptrace[par & 1][blockIdx.x][ev] = t;
+    if (ev == 0) g_ptrace[par & 1][blockIdx.x][4] = clock64();
+    if (ev == 3) g_ptrace[par & 1][blockIdx.x][5] = clock64();
+  }
+}
+#define PTRACE(ev)                                            \
+  do {                                                        \
+    if (threadIdx.x == 0) ptrace(launch_par, ev);             \
+  } while (0)
 #else
+#define PTRACE(ev) \
+  do {             \
+  } while (0)
 #define TRACE(ev, slot) \
   do {                  \
   } while (0)
@@ -383,6 +407,11 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
 
   const int warp = warp_id();
   const int lane = lane_id();
+  if (threadIdx.x == 0) TRACE(16, 0);
+#ifdef B200_TRACE
+  const unsigned launch_par = *reinterpret_cast<volatile unsigned*>(&g_plaunch);
+#endif
+  PTRACE(0);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -426,6 +455,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TRACE(16, 1);
   // PAIR: cluster rank (0 = leader: scheduler, MMA issuer, owner of the shared barriers);
   // `lead` maps one of this CTA's barriers to the leader's copy (shared::cluster address)
   const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
@@ -447,6 +477,8 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
   };
   griddep_wait();    // PDL: the prologue above overlapped the previous kernel; data access starts here
   griddep_launch();
+  if (threadIdx.x == 0) TRACE(16, 2);
+  PTRACE(1);
   // register hand-over (REG_SPLIT): each role adjusts its own limit at the top of its branch, so
   // the allocator never sees a join of the two limits
   auto regs_other = [] {
@@ -592,6 +624,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
         const int n_kv = n_kv_of(args.cu_seqlens[seq + 1] - seq_start, qblk);
         qb = (C::QBUF == 2) ? (k & 1) : 0;
         wait_cl(&q_full[qb], (C::QBUF == 2) ? ((k >> 1) & 1) : (k & 1));
+        if (k == 0 && lane == 0) TRACE(16, 3);
         // QK_t(s) of step s for tile t; per tile, step s uses S buffer (gt + s) % SB
         auto qk_step_tile = [&](int s, int t) {
           const int ki = rbase + 2 * s, kslot = ki % NS;
@@ -688,6 +721,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
         tc_fence_after();
         const uint32_t s_addr = s_base + C::S_COL(t, buf);
         if (row == 0 && hh == 0) TRACE(t, gt + j);
+        if (row == 0 && hh == 0 && t == 0 && k == 0 && j == 0) TRACE(16, 4);
         if (t == 0 && lane == 0 && warp < 4) TRACE(12 + warp, gt + j);
         const int kv0 = j * BN;
         const int kv0h = kv0 + hh * NCOL;  // first key of this thread's columns
@@ -754,6 +788,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
       }
 
       // ---------------------------------------------------------- epilogue for this item
+      if (row == 0 && hh == 0 && t == 0 && k == 0) TRACE(16, 5);
       float l_tot = l_run;
       if constexpr (SPLIT == 2) {
         xch[xidx(2, hh)] = l_run;
@@ -771,16 +806,28 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
         uint32_t r[32];
         tmem_ld32(o_addr + c * 32, r);
         if (valid) {
+          // 32-byte stores: a thread owns a whole output row, so each store fills one sector (the
+          // 16-byte form made the LSU split every warp store into 32 half-sector writes)
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const float* f = reinterpret_cast<const float*>(&r[v * 8]);
-            st_global_v4(orow + c * 32 + v * 8, pack_bf16x2(f[0] * inv_l, f[1] * inv_l),
-                         pack_bf16x2(f[2] * inv_l, f[3] * inv_l), pack_bf16x2(f[4] * inv_l, f[5] * inv_l),
-                         pack_bf16x2(f[6] * inv_l, f[7] * inv_l));
+          for (int v = 0; v < 2; ++v) {
+            uint32_t pk[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              pk[e] = pack_bf16x2(__uint_as_float(r[v * 16 + 2 * e]) * inv_l, __uint_as_float(r[v * 16 + 2 * e + 1]) * inv_l);
+            st_global_v8(orow + c * 32 + v * 16, pk);
           }
         }
       }
       tc_fence_before();
+      if (row == 0 && hh == 0 && t == 0 && k == 0) TRACE(16, 6);
+#ifdef B200_TRACE
+      if (row == 0 && hh == 0 && t == 0 && k == 0 && blockIdx.x < 1024) {
+        unsigned long long tn;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+        g_ptrace[launch_par & 1][blockIdx.x][6] = static_cast<unsigned long long>(w);
+        g_ptrace[launch_par & 1][blockIdx.x][7] = tn;
+      }
+#endif
       arrive_consumer(&o_free[t]);
       if (valid && hh == 0 && args.lse != nullptr) {
         args.lse[static_cast<size_t>(h) * args.total_tokens + seq_start + q_pos] =
@@ -795,6 +842,8 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
   tc_fence_before();
   __syncthreads();
   if constexpr (PAIR) cluster_sync_all();  // no remote arrive / MMA into the other CTA is in flight
+  if (threadIdx.x == 0) TRACE(16, 7);
+  PTRACE(2);
   if (warp == C::MMA_WARP) {
     __syncwarp();
     tc_fence_after();
@@ -811,8 +860,12 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
       args.sched[0] = 0;
       args.sched[2] = 0;
       __threadfence();
+#ifdef B200_TRACE
+      atomicAdd(&g_plaunch, 1u);
+#endif
     }
   }
+  PTRACE(3);
 }
 
 // Longest-first work list: one (seq, q block) entry per 128-row query block, sorted by causal

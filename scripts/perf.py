@@ -165,6 +165,76 @@ def cmd_trace(a):
     print("median cycles rel. to S0 of each step:", " ".join(f"{v:.0f}" for v in np.median(np.array(rows[5:]), 0)))
 
 
+def cmd_c1trace(a):
+    """CTA 0's first-item timeline on C1 (trace library): clock64 cycles from CTA entry to barriers
+    ready, past griddepcontrol.wait, Q seen by the MMA warp, first S, each step's S, epilogue, exit;
+    plus the host-side per-call time of a single launch."""
+    import numpy as np
+
+    lib = _native.load()
+    cfg = json.loads(a.cfg) if a.cfg else None
+    x = W.make_prefill(W.C1, device="cuda")
+    p = A.PrefillPlan(x.q, x.k, x.v, x.cu_seqlens, x.max_seqlen, config=cfg)
+    for _ in range(5):
+        p.run()
+        torch.cuda.synchronize()
+    buf = (ctypes.c_ulonglong * (17 * 512))()
+    lib.b200attn_debug_trace(buf, 17 * 512)
+    t = np.frombuffer(buf, dtype=np.uint64).reshape(17, 512).astype(np.int64)
+    e = t[16, :8] - t[16, 0]
+    names = ["entry", "ready", "griddep", "q_seen", "first_S", "epi_start", "epi_done", "exit"]
+    steps = [int(t[0, j] - t[16, 0]) for j in range(8) if t[0, j] > 0]
+    print(json.dumps({"tag": a.tag, "cfg": p.config, **{n: int(v) for n, v in zip(names, e)}, "S_steps": steps}), flush=True)
+
+
+def cmd_ptrace(a):
+    """K1 per-CTA %globaltimer stamps (trace library) of the last two of N graph-replayed launches:
+    kernel span, the gap between consecutive launches, and the spread of CTA entry / finish."""
+    import numpy as np
+
+    lib = _native.load()
+    lib.b200attn_debug_ptrace.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    cfg = json.loads(a.cfg) if a.cfg else None
+    for name in a.shapes.split(","):
+        x = W.make_prefill(SHAPES[name][1], device="cuda")
+        p = A.PrefillPlan(x.q, x.k, x.v, x.cu_seqlens, x.max_seqlen, config=cfg)
+        p.run()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(4):
+                p.run()
+        g.replay()
+        torch.cuda.synchronize()
+        buf = (ctypes.c_ulonglong * (2 * 1024 * 8))()
+        cnt = ctypes.c_uint(0)
+        assert lib.b200attn_debug_ptrace(buf, 2 * 1024 * 8, ctypes.byref(cnt)) == 0
+        t6 = np.frombuffer(buf, dtype=np.uint64).reshape(2, 1024, 8).astype(np.int64)
+        t = t6[:, :, :4]
+        last, prev = (cnt.value - 1) & 1, (cnt.value - 2) & 1
+        res = {"tag": a.tag, "shape": name, "cfg": p.config}
+        base = None
+        for lbl, par in (("prev", prev), ("last", last)):
+            tt = t[par]
+            tt = tt[tt[:, 0] > 0]
+            if base is None:
+                base = tt[:, 0].min()
+            r = (tt - base) / 1e3
+            res[lbl] = {"ctas": int(len(tt)), "entry": [round(float(r[:, 0].min()), 2), round(float(r[:, 0].max()), 2)],
+                        "griddep_max": round(float(r[:, 1].max()), 2), "done": [round(float(r[:, 2].min()), 2),
+                        round(float(np.median(r[:, 2])), 2), round(float(r[:, 2].max()), 2)],
+                        "exit_max": round(float(r[:, 3].max()), 2)}
+        cl = t6[prev][t6[prev][:, 0] > 0]
+        if a.per_cta:  # prev launch: per CTA [first item, entry, first-item epilogue done, done] (us)
+            b0 = cl[:, 0].min()
+            res["per_cta"] = sorted([[int(r[6]), round((r[0] - b0) / 1e3, 2), round((r[7] - b0) / 1e3, 2) if r[7] > r[0] else None,
+                                      round((r[2] - b0) / 1e3, 2)] for r in cl], key=lambda v: v[3])
+        res["sm_mhz_median"] = round(float(np.median((cl[:, 5] - cl[:, 4]) / np.maximum(cl[:, 3] - cl[:, 0], 1) * 1e3)), 1)
+        res["gap_us"] = round(res["last"]["entry"][0] - res["prev"]["exit_max"], 2)
+        res["span_us"] = round(res["last"]["exit_max"] - res["last"]["entry"][0], 2)
+        print(json.dumps(res), flush=True)
+
+
 def cmd_umma_rate(a):
     lib = _native.load()
     out = torch.zeros(148, dtype=torch.int64, device="cuda")
@@ -262,7 +332,7 @@ def cmd_e2e(a):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("cmd", choices=["time", "single", "prof", "trace", "umma-rate", "e2e", "dtrace"])
+    ap.add_argument("cmd", choices=["time", "single", "prof", "trace", "umma-rate", "e2e", "dtrace", "c1trace", "ptrace"])
     ap.add_argument("args", nargs="*")
     ap.add_argument("--op", default="prefill")
     ap.add_argument("--shapes", default="C3")
@@ -274,7 +344,8 @@ def main():
     ap.add_argument("--tag", default="")
     ap.add_argument("--per-cta", action="store_true", help="dtrace: per-CTA sm id / first S / last P")
     a = ap.parse_args()
-    {"time": cmd_time, "single": cmd_single, "prof": cmd_prof, "trace": cmd_trace, "umma-rate": cmd_umma_rate, "e2e": cmd_e2e, "dtrace": cmd_dtrace}[a.cmd](a)
+    {"time": cmd_time, "single": cmd_single, "prof": cmd_prof, "trace": cmd_trace, "umma-rate": cmd_umma_rate, "e2e": cmd_e2e, "dtrace": cmd_dtrace,
+     "c1trace": cmd_c1trace, "ptrace": cmd_ptrace}[a.cmd](a)
 
 
 if __name__ == "__main__":
