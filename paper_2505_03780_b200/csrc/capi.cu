@@ -242,9 +242,13 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
                                "cudaFuncSetAttribute(prefill)"))
     return rc0;
   const int D = 128;
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mq, mk, mv, mo;
   int rc;
   if ((rc = make_map_3d(&mq, p->q, D, p->num_q_heads, p->total_tokens, D * 2ull, (uint64_t)p->num_q_heads * D * 2,
+                        1, C::BM)))
+    return rc;
+  // O (TMA-store epilogue, C::STAGE_O): the same {64 d, 1 head, 128 tokens} box as Q
+  if ((rc = make_map_3d(&mo, p->o, D, p->num_q_heads, p->total_tokens, D * 2ull, (uint64_t)p->num_q_heads * D * 2,
                         1, C::BM)))
     return rc;
   // PAIR: each CTA of the pair loads BN/2 keys of a K tile (and 64 d columns of all BN keys of V)
@@ -298,10 +302,10 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   const long long items_ub = ((long long)p->total_tokens / 128 + p->num_seqs) * a.num_hg;
   if constexpr (PAIR) {
     const int pairs = (int)std::min<long long>(num_sms() / 2, std::max<long long>(1, items_ub));
-    e = launch_k_pair(kern, dim3(2 * pairs), dim3(C::NTHREADS), C::SMEM_BYTES, stream, mq, mk, mv, a);
+    e = launch_k_pair(kern, dim3(2 * pairs), dim3(C::NTHREADS), C::SMEM_BYTES, stream, mq, mk, mv, mo, a);
   } else {
     const int ctas = (int)std::min<long long>(num_sms(), std::max<long long>(1, items_ub));
-    e = launch_k(kern, dim3(ctas), dim3(C::NTHREADS), C::SMEM_BYTES, stream, mq, mk, mv, a);
+    e = launch_k(kern, dim3(ctas), dim3(C::NTHREADS), C::SMEM_BYTES, stream, mq, mk, mv, mo, a);
   }
   if (e != cudaSuccess) return cuda_fail(e, "prefill launch");
   return B200ATTN_OK;

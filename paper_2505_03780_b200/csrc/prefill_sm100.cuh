@@ -78,13 +78,52 @@ struct PrefillCfg {
   static constexpr int TILE_THREADS = 128 * SPLIT;           // softmax threads per Q tile
   static constexpr int TMA_WARP = NUM_SOFTMAX_WARPS;
   static constexpr int MMA_WARP = NUM_SOFTMAX_WARPS + 1;
+  static constexpr int Q_BYTES = BM * D * 2;   // 32 KB per Q tile (2 SW128 halves)
+  static constexpr int HALF_Q = BM * 128;
+  static constexpr int HALF_KV = BN * 128;     // V: offset of the second 64-column d block (unpaired)
+  static constexpr int HALF_K = PAIR ? (BN / 2) * 128 : BN * 128;  // K: offset of the second d half
+  // consumer arrivals on the leader's barriers: its own threads arrive locally, the peer's warps
+  // arrive remotely, one per warp
+  static constexpr int ARRIVE_P = PAIR ? TILE_THREADS + 4 : TILE_THREADS;  // p_full / o_free per tile
+  static constexpr int ARRIVE_ITEM_BASE = PAIR ? 2 + TILE_THREADS * NQ + 4 * NQ : 1 + TILE_THREADS * NQ;
+  static_assert(!PAIR || (SPLIT == 1 && BN == 128), "CTA pair: 4 softmax warps per tile, BLOCK_N = 128");
+  // Q is double-buffered when the ring leaves room: the next item's Q lands during this item
+  // SPLIT = 2: per-row exchange of half-row maxima (by step parity) and half-row sums
+  static constexpr int XCH_FLOATS = (SPLIT > 1) ? 3 * NQ * SPLIT * 128 : 0;
+  static constexpr int QBUF = (2 * NQ * Q_BYTES + (NSTAGE_CFG + 1) * 32768 + XCH_FLOATS * 4 <= 229376) ? 2 : 1;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_KV = OFF_Q + QBUF * NQ * Q_BYTES;
+  static constexpr int OFF_ITEM = OFF_KV + NSLOT * KV_BYTES;  // int32[2] work-item mailbox, +16: O-store mailbox
+  static constexpr int OFF_XCH = OFF_ITEM + 32;
+  static constexpr int OFF_BAR = OFF_XCH + XCH_FLOATS * 4;
+  // S_t is double-buffered when TMEM has room (NQ = 2 with BLOCK_N = 64, or NQ = 1): QK_t then runs
+  // two KV steps ahead of PV_t, so the softmax of step j+1 never waits for PV_t(j) + QK_t(j+1)
+  static constexpr int SB = (NQ * 2 * BN + NQ * 128 <= 512) ? 2 : 1;  // S buffers per tile
+  static constexpr int LA = SB;                                       // QK lookahead (KV steps)
+  // q_full[2], q_empty[2], kv_full/empty[NSLOT], s_full[NQ][SB], p_full[NQ][2], o_done[NQ][2],
+  // o_free[NQ], item_full/empty[2], drain, stage_full, stage_free
+  static constexpr int NUM_BARS = 4 + 2 * NSLOT + NQ * SB + 2 * NQ + 2 * NQ + NQ + 4 + 1 + 2;
+  // O epilogue through TMA stores (when 32 KB of shared memory are left): a tile's softmax threads
+  // write their rows of O (bf16, SW128 layout of two {64 d, 1 head, 128 tokens} boxes) into one
+  // staging buffer and a store warp issues the two TMA stores; the tiles take turns on the buffer.
+  // Blocks that end past their sequence (the last q block) are written row by row instead.
+  static constexpr int OFF_STAGE = (OFF_BAR + NUM_BARS * 8 + 16 + 1023) & ~1023;
+  // Enabled for the two-threads-per-row variants (num_warps = 8) only: A/B on one box (r2r), 16x2k
+  // 563 -> 535 us with BLOCK_M = 256, num_warps = 8; with one thread per row the staged epilogue
+  // cost C3 3.5% and C1 4% (the tiles queue on the one staging buffer, the store warp's hand-off
+  // lengthens C1's latency chain, and the extra code spills in the NQ = 2 kernel).
+  static constexpr bool STAGE_O = !PAIR && SPLIT == 2 && OFF_STAGE + BM * D * 2 + 1024 <= 232448;
+  static constexpr int SMEM_BYTES = STAGE_O ? OFF_STAGE + BM * D * 2 + 1024 : OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  static constexpr int ARRIVE_ITEM = ARRIVE_ITEM_BASE + (STAGE_O ? 1 : 0);  // + the store warp
   // Registers: the register file is split per SMSP (16K each) and warp w runs on SMSP w % 4, so
   // each SMSP holds NQ * SPLIT softmax warps + one producer-side warp.  When that leaves the softmax
   // warps short of registers, the producer side is padded to a full warpgroup (TMA, MMA, 2 idle
   // warps) that gives its registers to the softmax warpgroups with setmaxnreg.
   static constexpr int SM_PER_SMSP = NQ * SPLIT;
   static constexpr bool REG_SPLIT = SM_PER_SMSP == 2;  // at 4 per SMSP ptxas cannot fit the softmax in 120
-  static constexpr int NTHREADS = 32 * (NUM_SOFTMAX_WARPS + (REG_SPLIT ? 4 : 2));
+  // + a store warp (STAGE_O): the producer warpgroup's first idle warp, or one more warp
+  static constexpr int STORE_WARP = NUM_SOFTMAX_WARPS + 2;
+  static constexpr int NTHREADS = 32 * (NUM_SOFTMAX_WARPS + (REG_SPLIT ? 4 : (STAGE_O ? 3 : 2)));
   // setmaxnreg moves registers within the CTA's launch allocation (NTHREADS x the launch-bound
   // count, 65536 / NTHREADS rounded down to 8); an .inc beyond what the .dec warps released blocks
   // forever, so the softmax count is derived from that pool
@@ -98,32 +137,7 @@ struct PrefillCfg {
   static_assert(!REG_SPLIT || (REG_SOFTMAX >= REG_LAUNCH &&
                                32 * NUM_SOFTMAX_WARPS * REG_SOFTMAX + 128 * REG_OTHER <= NTHREADS * REG_LAUNCH),
                 "setmaxnreg split exceeds the launch allocation");
-  static constexpr int Q_BYTES = BM * D * 2;   // 32 KB per Q tile (2 SW128 halves)
-  static constexpr int HALF_Q = BM * 128;
-  static constexpr int HALF_KV = BN * 128;     // V: offset of the second 64-column d block (unpaired)
-  static constexpr int HALF_K = PAIR ? (BN / 2) * 128 : BN * 128;  // K: offset of the second d half
-  // consumer arrivals on the leader's barriers: its own threads arrive locally, the peer's warps
-  // arrive remotely, one per warp
-  static constexpr int ARRIVE_P = PAIR ? TILE_THREADS + 4 : TILE_THREADS;  // p_full / o_free per tile
-  static constexpr int ARRIVE_ITEM = PAIR ? 2 + TILE_THREADS * NQ + 4 * NQ : 1 + TILE_THREADS * NQ;
-  static_assert(!PAIR || (SPLIT == 1 && BN == 128), "CTA pair: 4 softmax warps per tile, BLOCK_N = 128");
-  // Q is double-buffered when the ring leaves room: the next item's Q lands during this item
-  // SPLIT = 2: per-row exchange of half-row maxima (by step parity) and half-row sums
-  static constexpr int XCH_FLOATS = (SPLIT > 1) ? 3 * NQ * SPLIT * 128 : 0;
-  static constexpr int QBUF = (2 * NQ * Q_BYTES + (NSTAGE_CFG + 1) * 32768 + XCH_FLOATS * 4 <= 229376) ? 2 : 1;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_KV = OFF_Q + QBUF * NQ * Q_BYTES;
-  static constexpr int OFF_ITEM = OFF_KV + NSLOT * KV_BYTES;  // int32[2] work-item mailbox
-  static constexpr int OFF_XCH = OFF_ITEM + 16;
-  static constexpr int OFF_BAR = OFF_XCH + XCH_FLOATS * 4;
-  // S_t is double-buffered when TMEM has room (NQ = 2 with BLOCK_N = 64, or NQ = 1): QK_t then runs
-  // two KV steps ahead of PV_t, so the softmax of step j+1 never waits for PV_t(j) + QK_t(j+1)
-  static constexpr int SB = (NQ * 2 * BN + NQ * 128 <= 512) ? 2 : 1;  // S buffers per tile
-  static constexpr int LA = SB;                                       // QK lookahead (KV steps)
-  // q_full[2], q_empty[2], kv_full/empty[NSLOT], s_full[NQ][SB], p_full[NQ][2], o_done[NQ][2],
-  // o_free[NQ], item_full/empty[2]
-  static constexpr int NUM_BARS = 4 + 2 * NSLOT + NQ * SB + 2 * NQ + 2 * NQ + NQ + 4 + 1;
-  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+
   static constexpr uint32_t TMEM_COLS = 512;
   __host__ __device__ static constexpr uint32_t S_COL(int t, int b) { return (t * SB + b) * BN; }
   __host__ __device__ static constexpr uint32_t O_COL(int t) { return NQ * SB * BN + t * 128; }
@@ -379,7 +393,8 @@ __device__ __forceinline__ void ptrace(unsigned par, int ev) {
 template <int NQ, int BN, int NSTAGE_CFG, int EMU, int SPLIT, bool PAIR = false>
 __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::NTHREADS, 1)
     prefill_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q, const __grid_constant__ CUtensorMap tmap_k,
-                       const __grid_constant__ CUtensorMap tmap_v, const PrefillKernelArgs args) {
+                       const __grid_constant__ CUtensorMap tmap_v, const __grid_constant__ CUtensorMap tmap_o,
+                       const PrefillKernelArgs args) {
   using C = PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>;
   constexpr int D = C::D, BM = C::BM, NS = C::NSLOT, NCOL = C::NCOL;
 
@@ -388,6 +403,8 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
   uint8_t* sQ = smem + C::OFF_Q;
   uint8_t* sKV = smem + C::OFF_KV;
   volatile int32_t* item_box = reinterpret_cast<volatile int32_t*>(smem + C::OFF_ITEM);
+  volatile int32_t* stage_box = item_box + 4;  // STAGE_O: {block needs no TMA store, first token, q head}
+  uint8_t* sStage = smem + C::OFF_STAGE;
   float* xch = reinterpret_cast<float*>(smem + C::OFF_XCH);  // [3][NQ][SPLIT][128]: max (2 parities), sum
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars;       // [2]
@@ -403,6 +420,8 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
   uint64_t* item_full = o_free + NQ;       // [2]
   uint64_t* item_empty = item_full + 2;
   uint64_t* drain = item_empty + 2;         // PAIR: the leader's MMA warp waits its last MMAs out
+  uint64_t* stage_full = drain + 1;         // STAGE_O: a tile's O rows are in the staging buffer
+  uint64_t* stage_free = stage_full + 1;    // STAGE_O: the TMA store has read the staging buffer
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS);
 
   const int warp = warp_id();
@@ -435,6 +454,8 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
       mbar_init(&item_empty[i], C::ARRIVE_ITEM);
     }
     mbar_init(drain, 1);
+    mbar_init(stage_full, C::TILE_THREADS);
+    mbar_init(stage_free, 1);
     fence_barrier_init();
   }
   if (warp == C::MMA_WARP) {
@@ -447,6 +468,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
     tma_prefetch_desc(&tmap_q);
     tma_prefetch_desc(&tmap_k);
     tma_prefetch_desc(&tmap_v);
+    if constexpr (C::STAGE_O) tma_prefetch_desc(&tmap_o);
   }
   tc_fence_before();
   if constexpr (PAIR)
@@ -670,6 +692,34 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
         mbar_wait(drain, 0);
       }
     }
+  } else if (C::STAGE_O && warp == C::STORE_WARP) {
+    // ------------------------------------------------------------ O store warp (STAGE_O)
+    // per item, the NQ tiles' epilogues in order (use n = NQ * item + tile): wait for the rows in
+    // the staging buffer, issue the two {64 d, 1, 128} TMA stores, free the buffer once TMA read it
+    regs_other();
+    int n = 0;
+    for (int k = 0;; ++k) {
+      mbar_wait(&item_full[k & 1], (k >> 1) & 1);
+      const int w = item_box[k & 1];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&item_empty[k & 1]);
+      if (w < 0) break;
+      for (int t = 0; t < NQ; ++t, ++n) {
+        mbar_wait(stage_full, n & 1);
+        const int skip = stage_box[0], row0 = stage_box[1], head = stage_box[2];
+        if (lane == 0) {
+          if (!skip) {
+            tma_store_3d(&tmap_o, sStage, 0, head, row0);
+            tma_store_3d(&tmap_o, sStage + C::HALF_Q, 64, head, row0);
+            bulk_commit();
+            bulk_wait_read_all();
+          }
+          mbar_arrive(stage_free);
+        }
+        __syncwarp();
+      }
+    }
+    if (lane == 0) bulk_wait_all();  // the output is written before the CTA retires
   } else if (warp < C::NUM_SOFTMAX_WARPS) {
     // ------------------------------------------------------------ softmax warps of tile t
     if constexpr (C::REG_SPLIT) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::REG_SOFTMAX));
@@ -801,11 +851,29 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
       const bool valid = q_pos < seq_len;
       const float inv_l = (l_tot > 0.f) ? 1.f / l_tot : 0.f;
       __nv_bfloat16* orow = args.o + (static_cast<size_t>(seq_start + q_pos) * args.num_q_heads + h) * D + hh * OCOLS;
+      // STAGE_O: whole blocks go through the staging buffer and a TMA store; the last (partial)
+      // block of a sequence is written row by row (a box store would spill into the next sequence)
+      const bool staged = C::STAGE_O && (qblk * BM + BM <= seq_len);
+      if constexpr (C::STAGE_O) {
+        const int n = NQ * k + t;  // this tile's turn on the staging buffer
+        if (n > 0) mbar_wait(stage_free, (n - 1) & 1);
+      }
 #pragma unroll
       for (int c = 0; c < OCOLS / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(o_addr + c * 32, r);
-        if (valid) {
+        if (staged) {
+          // row `row` of the SW128 box pair: 16-byte unit j of a 128-byte half-row at j ^ (row & 7)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int col = hh * OCOLS + c * 32 + u * 8;  // first of 8 bf16
+            const int hf = col >> 6, j = (col & 63) >> 3;
+            const uint32_t a = smem_u32(sStage) + hf * C::HALF_Q + row * 128 + ((j ^ (row & 7)) << 4);
+            const float* f = reinterpret_cast<const float*>(&r[u * 8]);
+            st_shared_v4(a, pack_bf16x2(f[0] * inv_l, f[1] * inv_l), pack_bf16x2(f[2] * inv_l, f[3] * inv_l),
+                         pack_bf16x2(f[4] * inv_l, f[5] * inv_l), pack_bf16x2(f[6] * inv_l, f[7] * inv_l));
+          }
+        } else if (valid) {
           // 32-byte stores: a thread owns a whole output row, so each store fills one sector (the
           // 16-byte form made the LSU split every warp store into 32 half-sector writes)
 #pragma unroll
@@ -817,6 +885,15 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
             st_global_v8(orow + c * 32 + v * 16, pk);
           }
         }
+      }
+      if constexpr (C::STAGE_O) {
+        if (staged) fence_proxy_async_smem();  // generic smem writes -> visible to the TMA store
+        if (row == 0 && hh == 0) {
+          stage_box[0] = staged ? 0 : 1;
+          stage_box[1] = seq_start + qblk * BM;
+          stage_box[2] = h;
+        }
+        mbar_arrive(stage_full);
       }
       tc_fence_before();
       if (row == 0 && hh == 0 && t == 0 && k == 0) TRACE(16, 6);
