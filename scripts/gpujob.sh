@@ -17,6 +17,10 @@
 #   flatsweep  K2' CTA count (min tiles per CTA) x fused/K3' merge on small decode shapes
 #   pdlab      PDL on/off on latency-bound shapes      dtrace  K2' per-CTA timelines (trace library)
 #   narrow     K2' vs K2 on kv-head shards (Hkv = 1/2/4) and batch 4096     e2e   perf.py e2e breakdown
+#   libab      two library builds A/B on one box      ptrace  K1 per-CTA launch timelines + C1 trace (trace build)
+#   umma       tcgen05 MMA issue-rate probe            c5      the C5 sweep (unmodified ktune tune, exhaustive)
+#   pairtests / pairab   CTA-pair K1 parity / A/B      bandtests / bandab   banded K1 order parity / A/B
+#   smalldec / mergesmall   small decode shapes (dispatch vs K2', per-CTA timelines), merge modes
 set -u
 TAG=$1; shift
 mkdir -p gpurun_out
@@ -81,12 +85,6 @@ for r in "$@"; do
               for v in "B200ATTN_FLAT_MERGE=0" "B200ATTN_FLAT_MERGE=1" "B200ATTN_FLAT_MERGE=0 B200ATTN_PDL_COMBINE=1" "B200ATTN_PDL=0"; do
                 env $v timeout 300 python scripts/perf.py time --op decode --shapes $S --cfg "$C" --tag "$v"; done; } > ${O}_mergesmall.log 2>&1
             cat ${O}_mergesmall.log ;;
-    dyntests) timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_api.py -m gpu -q -x \
-             -k "decode or flat or C2 or C4 or c2 or c4 or step" > ${O}_dyntests.log 2>&1; tail -8 ${O}_dyntests.log ;;
-    dynab) S=C2,C4shard,C2fp8,d64x512,d16x2k,C2kv2,C4kv1; C='{"TILE_N": 16, "num_splits": 0, "num_stages": 4}'
-            for v in 0 1 0 1; do B200ATTN_FLAT_DYN=$v timeout 300 python scripts/perf.py time --op decode --shapes $S --tag "dyn$v"; done > ${O}_dynab.log 2>&1
-            for v in 0 1; do B200ATTN_FLAT_DYN=$v timeout 300 python scripts/perf.py time --op decode --shapes C2,C4shard --partial --tag "K2only-dyn$v"; done >> ${O}_dynab.log 2>&1
-            cat ${O}_dynab.log ;;
     pairtests) timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "pair or every_compiled" \
              > ${O}_pairtests.log 2>&1; tail -15 ${O}_pairtests.log ;;
     pairab) for c in '{"BLOCK_M": 256, "BLOCK_N": 128, "num_warps": 4, "num_stages": 3, "waves_per_eu": 1, "PRE_LOAD_V": false}' \
