@@ -221,9 +221,9 @@ def cmd_post(a):
         md.append("")
     table_path = ROOT / "paper_2505_03780_b200" / "dispatch_table.json"
     if rows_table and table_path.exists():
-        # an op that was not re-swept keeps its rows from the shipped table
-        done_ops = {r["shape"]["op"] for r in rows_table}
-        kept = [r for r in json.loads(table_path.read_text())["rows"] if r["shape"]["op"] not in done_ops]
+        # shapes that were not re-swept (another op, or a sweep cut short) keep their shipped rows
+        done = {json.dumps(r["shape"], sort_keys=True) for r in rows_table}
+        kept = [r for r in json.loads(table_path.read_text())["rows"] if json.dumps(r["shape"], sort_keys=True) not in done]
         rows_table = kept + rows_table
     if rows_table:
         table_path.write_text(json.dumps({"source": "ktune tune --strategy exhaustive (scripts/c5_sweep.py)",

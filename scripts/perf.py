@@ -49,6 +49,7 @@ SHAPES = {
     "d64x512": ("decode", dict(W.C2, batch_size=64, seq_len=512)),
     "d1x2k": ("decode", dict(W.C2, batch_size=1, seq_len=2048)), "d4x512": ("decode", dict(W.C2, batch_size=4, seq_len=512)),
     "d16x2k": ("decode", dict(W.C2, batch_size=16, seq_len=2048)), "d1x128": ("decode", dict(W.C2, batch_size=1, seq_len=128)),
+    "d16x128": ("decode", dict(W.C2, batch_size=16, seq_len=128)),
 }
 
 
