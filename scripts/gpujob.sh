@@ -85,13 +85,6 @@ for r in "$@"; do
               for v in "B200ATTN_FLAT_MERGE=0" "B200ATTN_FLAT_MERGE=1" "B200ATTN_FLAT_MERGE=0 B200ATTN_PDL_COMBINE=1" "B200ATTN_PDL=0"; do
                 env $v timeout 300 python scripts/perf.py time --op decode --shapes $S --cfg "$C" --tag "$v"; done; } > ${O}_mergesmall.log 2>&1
             cat ${O}_mergesmall.log ;;
-    clusab) S=d1x128,d1x512,d1x2k,d4x512,d4x2k,d16x128,d1x8k,d16x512,C2
-            for r in 1 2; do for v in 0 auto 1; do
-              env $( [ $v != auto ] && echo B200ATTN_SPLIT_CLUSTER=$v ) timeout 300 python scripts/perf.py time --op decode \
-                --shapes $S --tag "cluster=$v"
-            done; done > ${O}_clusab.log 2>&1; cat ${O}_clusab.log ;;
-    clustests) timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_api.py -m gpu -q -x \
-             -k "decode or cluster or step" > ${O}_clustests.log 2>&1; tail -12 ${O}_clustests.log ;;
     pairtests) timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "pair or every_compiled" \
              > ${O}_pairtests.log 2>&1; tail -15 ${O}_pairtests.log ;;
     pairab) for c in '{"BLOCK_M": 256, "BLOCK_N": 128, "num_warps": 4, "num_stages": 3, "waves_per_eu": 1, "PRE_LOAD_V": false}' \
