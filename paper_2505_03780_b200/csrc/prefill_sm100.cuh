@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
       const int total_work = (args.single_nqb > 0 ? args.single_nqb : args.sched[1]) * args.num_hg;
       const uint64_t keep = policy_evict_last();  // K/V tiles are re-read by other q blocks / heads
       int ri = 0;
-      const uint64_t once = policy_evict_first();  // Q tiles are read by one item only
+      [[maybe_unused]] const uint64_t once = PAIR ? policy_evict_first() : 0;  // PAIR: Q tiles are read once
       for (int k = 0;; ++k) {
         int w;
         if (!PAIR || rank == 0) {
