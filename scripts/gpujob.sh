@@ -85,6 +85,21 @@ for r in "$@"; do
               for v in "B200ATTN_FLAT_MERGE=0" "B200ATTN_FLAT_MERGE=1" "B200ATTN_FLAT_MERGE=0 B200ATTN_PDL_COMBINE=1" "B200ATTN_PDL=0"; do
                 env $v timeout 300 python scripts/perf.py time --op decode --shapes $S --cfg "$C" --tag "$v"; done; } > ${O}_mergesmall.log 2>&1
             cat ${O}_mergesmall.log ;;
+    libab) # two builds on one box, alternating (base = _lib/libb200attn_base.so): LIBAB_OP / LIBAB_SHAPES
+            for r in 1 2; do for lib in base new; do
+              f=$PWD/paper_2505_03780_b200/_lib/libb200attn.so; [ $lib = base ] && f=$PWD/paper_2505_03780_b200/_lib/libb200attn_base.so
+              B200ATTN_LIB=$f timeout 600 python scripts/perf.py time --op ${LIBAB_OP:-prefill} \
+                --shapes ${LIBAB_SHAPES:-C1,C3,1x16k,16x2k,16x8k} --tag $lib
+            done; done > ${O}_libab.log 2>&1; cat ${O}_libab.log ;;
+    ptrace) T=$PWD/paper_2505_03780_b200/_lib/libb200attn_trace.so  # K1 per-CTA launch timelines (trace build)
+            for pdl in 1 0; do B200ATTN_PDL=$pdl B200ATTN_LIB=$T timeout 300 python scripts/perf.py ptrace \
+              --shapes C1,C3,1x16k --tag "pdl$pdl"; done > ${O}_ptrace.log 2>&1
+            B200ATTN_PDL=0 B200ATTN_LIB=$T timeout 300 python scripts/perf.py ptrace --shapes C1 --tag pdl0 --per-cta >> ${O}_ptrace.log 2>&1
+            B200ATTN_LIB=$T timeout 300 python scripts/perf.py c1trace --tag pdl1 >> ${O}_ptrace.log 2>&1
+            cat ${O}_ptrace.log ;;
+    umma) timeout 300 python scripts/perf.py umma-rate > ${O}_umma.log 2>&1; cat ${O}_umma.log ;;
+    c5) timeout 5400 python scripts/c5_sweep.py run --out ${O}_c5 --batch 4 > ${O}_c5_run.log 2>&1
+        rm -rf ${O}_c5/cache; tail -5 ${O}_c5_run.log ;;
     pairtests) timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "pair or every_compiled" \
              > ${O}_pairtests.log 2>&1; tail -15 ${O}_pairtests.log ;;
     pairab) for c in '{"BLOCK_M": 256, "BLOCK_N": 128, "num_warps": 4, "num_stages": 3, "waves_per_eu": 1, "PRE_LOAD_V": false}' \
