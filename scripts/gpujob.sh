@@ -45,9 +45,16 @@ for r in "$@"; do
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${O}_launches_prefill.csv \
         python bench.py --workload prefill --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 ;;
     ncupf) timeout 900 ncu --set full --clock-control none --import-source on -k regex:prefill_fwd -s 2 -c 1 \
-             -o ${O}_pf python scripts/perf.py prof --op prefill > ${O}_ncupf.log 2>&1; tail -3 ${O}_ncupf.log ;;
+             -o ${O}_pf python scripts/perf.py prof --op prefill > ${O}_ncupf.log 2>&1; tail -3 ${O}_ncupf.log
+           # summarised on the box (a full report can push gpurun_out past its copy-back limit)
+           python scripts/ncu_summarize.py full ${O}_pf.ncu-rep prefill_fwd_kernel 1291603001344 flops > ${O}_ncupf_summary.txt 2>&1
+           ncu -i ${O}_pf.ncu-rep --page raw --csv > ${O}_ncupf_raw.csv 2>/dev/null
+           [ -n "${NCU_DROP_REP:-}" ] && rm -f ${O}_pf.ncu-rep ;;
     ncudec) timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_flat -s 2 -c 1 \
-             -o ${O}_dec python scripts/perf.py prof --op decode > ${O}_ncudec.log 2>&1; tail -3 ${O}_ncudec.log ;;
+             -o ${O}_dec python scripts/perf.py prof --op decode > ${O}_ncudec.log 2>&1; tail -3 ${O}_ncudec.log
+           python scripts/ncu_summarize.py full ${O}_dec.ncu-rep decode_flat_kernel 1074856192 bytes > ${O}_ncudec_summary.txt 2>&1
+           ncu -i ${O}_dec.ncu-rep --page raw --csv > ${O}_ncudec_raw.csv 2>/dev/null
+           [ -n "${NCU_DROP_REP:-}" ] && rm -f ${O}_dec.ncu-rep ;;
     sanitize) timeout 2400 bash scripts/sanitize.sh ${O}_sanitize ;;
     sota) timeout 2400 python scripts/sota.py --out ${O}_sota.json > ${O}_sota.log 2>&1; tail -30 ${O}_sota.log ;;
     sotagrid) timeout 2400 python scripts/sota.py --grid --out ${O}_sotagrid.json > ${O}_sotagrid.log 2>&1; tail -3 ${O}_sotagrid.log ;;
