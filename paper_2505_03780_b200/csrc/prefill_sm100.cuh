@@ -706,8 +706,8 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
       if (w < 0) break;
       for (int t = 0; t < NQ; ++t, ++n) {
         mbar_wait(stage_full, n & 1);
-        const int skip = stage_box[0], row0 = stage_box[1], head = stage_box[2];
-        if (lane == 0) {
+        if (lane == 0) {  // only the issuing lane reads the mailbox: it is rewritten once stage_free fires
+          const int skip = stage_box[0], row0 = stage_box[1], head = stage_box[2];
           if (!skip) {
             tma_store_3d(&tmap_o, sStage, 0, head, row0);
             tma_store_3d(&tmap_o, sStage + C::HALF_Q, 64, head, row0);
