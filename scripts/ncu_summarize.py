@@ -19,8 +19,10 @@ WANT = {
     "dram__bytes_read.sum": "dram_read",
     "dram__bytes_write.sum": "dram_write",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct_of_peak",
-    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_pct",
-    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_pct",
+    # tensor pipe busy cycles as a share of the SM's active cycles (the one tensor-pipe figure quoted)
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pipe_pct",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "mufu_pipe_pct",
+    "lts__t_sector_hit_rate.pct": "l2_hit_pct",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
     "launch__registers_per_thread": "registers",
     "launch__grid_size": "grid",
@@ -36,7 +38,11 @@ SCALE = {"ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1, "byte": 1, "Kbyte": 1e3, "M
 
 
 def raw_rows(rep):
-    txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """rows of `ncu -i REP --page raw --csv`, or of that export itself when REP is a .csv"""
+    if str(rep).endswith(".csv"):
+        txt = Path(rep).read_text()
+    else:
+        txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     return rows[0], rows[1], rows[2:]
 
@@ -59,7 +65,8 @@ def full(rep, key, work, kind):
     rec = {"source": str(rep), "kernel_name": m["kernel_name"][:160], "duration_s": m.get("duration"),
            "dram_bytes_per_launch": dram, "dram_read": m.get("dram_read"), "dram_write": m.get("dram_write"),
            "dram_pct_of_peak": m.get("dram_pct_of_peak"), "tensor_pipe_pct": m.get("tensor_pipe_pct"),
-           "sm_throughput_pct": m.get("sm_throughput_pct"), "registers": m.get("registers"), "grid": m.get("grid"),
+           "sm_throughput_pct": m.get("sm_throughput_pct"), "mufu_pipe_pct": m.get("mufu_pipe_pct"),
+           "l2_hit_pct": m.get("l2_hit_pct"), "registers": m.get("registers"), "grid": m.get("grid"),
            "block": m.get("block"), "l2_bytes": m.get("l2_bytes"), "sm_clock_hz": m.get("sm_hz"),
            "note": "ncu --set full --clock-control none (serialised, cold-cache replay)"}
     work = float(work)
