@@ -261,9 +261,12 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   int nkeys = 0;
   prefill_ws_ints(p, &nkeys);
   int32_t* ws = reinterpret_cast<int32_t*>(p->workspace);
-  // one sequence: its q blocks in reverse are already longest-first, so no schedule kernel; the
-  // kernel's last CTA re-zeroes the work counter (the workspace starts zeroed, see header)
-  const bool single = (p->num_seqs == 1);
+  // one sequence, or sequences of equal length (total = num_seqs x max_seqlen forces every length to
+  // max_seqlen): the kernel decodes items analytically, q blocks longest first across the sequences,
+  // so no schedule kernel (a launch and a dependent round trip saved on small batches); the kernel's
+  // last CTA re-zeroes the work counter (the workspace starts zeroed, see header)
+  const bool single = p->num_seqs == 1 ||
+                      (p->max_seqlen > 0 && (long long)p->num_seqs * p->max_seqlen == (long long)p->total_tokens);
   const int band = prefill_band(p);
   cudaError_t e;
   if (!single && band > 0) {
@@ -293,6 +296,7 @@ int launch_prefill(const b200attn_prefill_params* p, cudaStream_t stream) {
   a.causal = p->causal;
   a.num_hg = p->num_q_heads / (NQ * (PAIR ? 2 : 1));
   a.single_nqb = single ? (p->max_seqlen + C::BM - 1) / C::BM : 0;
+  a.useqs = single ? p->num_seqs : 0;
   const float scale = p->softmax_scale > 0.f ? p->softmax_scale : 1.0f / sqrtf((float)p->head_dim);
   a.scale_log2 = scale * 1.4426950408889634f;
   a.speculate = prefill_speculate() ? 1 : 0;

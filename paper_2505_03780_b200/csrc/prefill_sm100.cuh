@@ -44,8 +44,10 @@ struct PrefillKernelArgs {
   int32_t group;  // Hq / Hkv
   int32_t causal;
   int32_t num_hg;    // Hq / NQ head groups per (seq, q block)
-  int32_t single_nqb;  // > 0: one sequence with this many q blocks -> no schedule kernel, items are
-                       // q blocks longest first; the work counter is then reset by the last CTA
+  int32_t single_nqb;  // > 0: uniform batch — `useqs` sequences of this many q blocks each (one
+                       // sequence, or equal lengths): no schedule kernel, items are decoded
+                       // analytically, q blocks longest first across the sequences
+  int32_t useqs;
   float scale_log2;  // softmax_scale * log2(e)
   int32_t speculate;  // 1: interior tiles take the single-pass path against the running max
   // L2-aware order (band > 0; problems whose K/V exceeds ~half of L2): q blocks are taken in bands
@@ -190,16 +192,19 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float& y0, float&
 __device__ __forceinline__ void prefill_decode_item(int w, const PrefillKernelArgs& a, int& seq, int& qblk,
                                                     int& hg) {
   if (a.band > 0) {
-    if (a.single_nqb > 0) {  // bands from the top q block down; all but the last are full
-      const int per_band = a.band * a.num_hg;
+    if (a.single_nqb > 0) {  // bands from the top q block down (all but the last are full); inside a
+                             // band by sequence, kv head, q block descending
+      const int per_band = a.band * a.useqs * a.num_hg;
       const int i = w / per_band;
       const int r = w - i * per_band;
       const int nq = min(a.band, a.single_nqb - i * a.band);
+      const int per_seq = nq * a.num_hg;
+      seq = r / per_seq;
+      const int r1 = r - seq * per_seq;
       const int per_kvh = nq * a.hpk;
-      const int kvh = r / per_kvh;
-      const int r2 = r - kvh * per_kvh;
+      const int kvh = r1 / per_kvh;
+      const int r2 = r1 - kvh * per_kvh;
       const int e = r2 / a.hpk;
-      seq = 0;
       qblk = a.single_nqb - 1 - i * a.band - e;
       hg = kvh * a.hpk + (r2 - e * a.hpk);
     } else {
@@ -213,9 +218,15 @@ __device__ __forceinline__ void prefill_decode_item(int w, const PrefillKernelAr
   }
   const int pair = w / a.num_hg;
   hg = w - pair * a.num_hg;
-  if (a.single_nqb > 0) {
-    seq = 0;
-    qblk = a.single_nqb - 1 - pair;
+  if (a.single_nqb > 0) {  // uniform batch: q block index descending, sequences minor
+    if (a.useqs == 1) {      // one sequence (no integer division on the latency-bound path)
+      seq = 0;
+      qblk = a.single_nqb - 1 - pair;
+      return;
+    }
+    const int r = pair / a.useqs;
+    seq = pair - r * a.useqs;
+    qblk = a.single_nqb - 1 - r;
     return;
   }
   const uint32_t it = static_cast<uint32_t>(a.items[pair]);  // (seq << 16) | q block, seq < 65536
@@ -516,7 +527,7 @@ __global__ void __launch_bounds__(PrefillCfg<NQ, BN, NSTAGE_CFG, SPLIT, PAIR>::N
     // ------------------------------------------------------------ scheduler + TMA producer
     regs_other();
     if (lane == 0) {
-      const int total_work = (args.single_nqb > 0 ? args.single_nqb : args.sched[1]) * args.num_hg;
+      const int total_work = (args.single_nqb > 0 ? args.single_nqb * args.useqs : args.sched[1]) * args.num_hg;
       const uint64_t keep = policy_evict_last();  // K/V tiles are re-read by other q blocks / heads
       int ri = 0;
       [[maybe_unused]] const uint64_t once = PAIR ? policy_evict_first() : 0;  // PAIR: Q tiles are read once

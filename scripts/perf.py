@@ -35,6 +35,8 @@ SHAPES = {
     "4x8k": ("prefill", dict(W.C1, batch_size=4, seq_len=8192)),
     "16x8k": ("prefill", dict(W.C1, batch_size=16, seq_len=8192)), "1x32k": ("prefill", dict(W.C1, seq_len=32768)),
     "16x2k": ("prefill", dict(W.C1, batch_size=16, seq_len=2048)),
+    "4x128": ("prefill", dict(W.C1, batch_size=4, seq_len=128)), "16x128": ("prefill", dict(W.C1, batch_size=16, seq_len=128)),
+    "4x512": ("prefill", dict(W.C1, batch_size=4, seq_len=512)), "64x512": ("prefill", dict(W.C1, batch_size=64, seq_len=512)),
     "C2": ("decode", W.C2), "C4shard": ("decode", dict(W.C4, batch_size=32)),
     "C2fp8": ("decode", dict(W.C2, kv_dtype="fp8_e4m3")), "b1x32k": ("decode", dict(W.C2, batch_size=1, seq_len=32768)),
     # kv-head shards (one GPU's share when the kv heads are split): C2 over 4 / 8 GPUs, C4 over 8

@@ -268,6 +268,17 @@ def test_prefill_every_compiled_variant(bm, bn, ns, nw, pair):
     check(f"prefill variant {bm}/{bn}/{ns}/w{nw}{'/pair' if pair else ''}", out, ref, base)
 
 
+@pytest.mark.parametrize("cfg", [pcfg(), pcfg(128, 128, 3), pcfg(256, 128, 2, nw=8), pcfg(256, 128, 2, pair=True)],
+                         ids=["bm256", "bm128", "bm256w8", "pair"])
+@pytest.mark.parametrize("lens", [[128] * 16, [300] * 5, [1] * 7, [1024] * 3], ids=lambda l: f"{len(l)}x{l[0]}")
+def test_prefill_uniform_batch(cfg, lens):
+    """Equal-length batches take the analytic item order (no schedule kernel): ragged last q blocks,
+    single tokens, many short sequences; causal and not."""
+    for causal in (True, False):
+        out, ref, base = run_prefill(lens, cfg=cfg, causal=causal)
+        check(f"prefill uniform {len(lens)}x{lens[0]} causal={causal}", out, ref, base)
+
+
 # ------------------------------------------------------------------ CTA pair (cta_group::2) variants
 PAIR_CFGS = [pcfg(256, 128, 2, pair=True), pcfg(128, 128, 2, pair=True)]
 
@@ -826,6 +837,7 @@ def test_prefill_banded_order_forced(tmp_path, band):
     (schedule kernel) and single-sequence (analytic) item decoding, causal and not, GQA 4 and 8,
     BLOCK_M 128/256 and the CTA pair; every case vs the oracle."""
     cases = [([300, 77, 1000, 129, 1], 32, 8, True, pcfg()), ([1000], 32, 8, True, pcfg()),
+             ([700] * 3, 32, 8, True, pcfg()), ([520] * 4, 16, 2, False, pcfg(128, 128, 3)),
              ([700, 129], 16, 2, True, pcfg(128, 128, 2)), ([900], 16, 2, False, pcfg(128, 128, 3)),
              ([500, 1, 640], 32, 8, False, pcfg()), ([1000, 260], 32, 4, True, pcfg(256, 128, 2, pair=True)),
              ([1100], 32, 4, True, pcfg(256, 128, 2, pair=True))]

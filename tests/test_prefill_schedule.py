@@ -7,17 +7,24 @@ import itertools
 import pytest
 
 
-def decode_single(w, nqb, band, num_hg, hpk):
-    """prefill_decode_item, band > 0, one sequence (analytic, bands from the top q block down)."""
-    per_band = band * num_hg
+def decode_single(w, nqb, band, num_hg, hpk, useqs=1):
+    """prefill_decode_item for a uniform batch (`useqs` sequences of nqb q blocks; analytic).
+    band > 0: bands from the top q block down, inside a band by sequence, kv head, q block
+    descending; band == 0: q block descending, sequences minor."""
+    if band == 0:
+        pair, hg = divmod(w, num_hg)
+        r, seq = divmod(pair, useqs)
+        return seq, nqb - 1 - r, hg
+    per_band = band * useqs * num_hg
     i = w // per_band
     r = w - i * per_band
     nq = min(band, nqb - i * band)
+    seq, r1 = divmod(r, nq * num_hg)
     per_kvh = nq * hpk
-    kvh = r // per_kvh
-    r2 = r - kvh * per_kvh
+    kvh = r1 // per_kvh
+    r2 = r1 - kvh * per_kvh
     e = r2 // hpk
-    return 0, nqb - 1 - i * band - e, kvh * hpk + (r2 - e * hpk)
+    return seq, nqb - 1 - i * band - e, kvh * hpk + (r2 - e * hpk)
 
 
 def schedule_banded(lens, causal, hkv, band):
@@ -55,6 +62,19 @@ def test_single_sequence_banded_decode_is_a_bijection(nqb, band, hkv, hpk):
     # consecutive items of one kv head share its K/V stream: head groups of a kv head are adjacent
     for w in range(0, len(items), hpk):
         assert len({items[w + j][2] // hpk for j in range(hpk)}) == 1
+
+
+@pytest.mark.parametrize("nqb,band,hkv,hpk,useqs", [(4, 0, 8, 2, 4), (1, 0, 8, 1, 16), (64, 32, 8, 2, 16), (9, 4, 2, 4, 3),
+                                                   (37, 0, 4, 2, 5)])
+def test_uniform_batch_decode_is_a_bijection(nqb, band, hkv, hpk, useqs):
+    """Equal-length batches (no schedule kernel): every (sequence, q block, head group) exactly once,
+    longest q blocks first (band 0) or longest band first."""
+    num_hg = hkv * hpk
+    items = [decode_single(w, nqb, band, num_hg, hpk, useqs) for w in range(nqb * useqs * num_hg)]
+    assert sorted(items) == sorted((s, q, h) for s in range(useqs) for q in range(nqb) for h in range(num_hg))
+    # bands are anchored at the top q block: band index (nqb - 1 - q) // band never decreases
+    key = [nqb - 1 - q if band == 0 else (nqb - 1 - q) // band for _, q, _ in items]
+    assert all(a <= b for a, b in itertools.pairwise(key))
 
 
 @pytest.mark.parametrize("causal", [True, False])
