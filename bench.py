@@ -606,9 +606,15 @@ def e2e_decode(d, dev, world, stream, n_steps, chunks=0):
     return {"value": world * d.kv_bytes / (e_ms / 1e3) / 1e9, "unit": "GB/s",
             "h2d_bytes_per_step": step.h2d_bytes, "d2h_bytes_per_step": step.d2h_bytes, "ms_per_step": e_ms,
             "chunks": step.chunks,
-            "path": "paper_2505_03780_b200.DecodeStep (public API: one CUDA graph of H2D copy from pinned host "
-                    "memory -> cache_append -> paged_decode -> D2H copy of the output, the batch in chunks whose "
-                    "copies overlap the other chunks' kernels); paged KV pool and block table resident in HBM"}, out
+            "zero_copy": step.zero_copy,
+            "path": ("paper_2505_03780_b200.DecodeStep (public API, one CUDA graph): an ingest kernel reads the "
+                     "step's q / seq_lens / new K,V / slots from pinned host memory over PCIe (q, seq_lens -> HBM; "
+                     "K,V appended into their pages) -> paged_decode (K2' + K3') writing the output rows straight "
+                     "into pinned host memory; paged KV pool and block table resident in HBM"
+                     if step.zero_copy else
+                     "paper_2505_03780_b200.DecodeStep (public API: one CUDA graph of H2D copy from pinned host "
+                     "memory -> cache_append -> paged_decode -> D2H copy of the output, the batch in chunks whose "
+                     "copies overlap the other chunks' kernels); paged KV pool and block table resident in HBM")}, out
 
 
 # ----------------------------------------------------------------------------- the B200 arm
@@ -778,7 +784,10 @@ def run_b200(args, world, rank, local, gpu):
             t8 = cuda_time(g8.replay, 10, stream) / 10
             extra["decode_C2_fp8_kv"] = {"GB/s": d8.total_bytes / (t8 / 1e3) / 1e9, "ms": t8,
                                          "frac_of_measured_hbm": d8.total_bytes / (t8 / 1e3) / 1e9 / pk["hbm_gbs"],
-                                         "kv_bytes": d8.kv_bytes, "speedup_vs_bf16_kv": (ms / args.steps) / t8,
+                                         "kv_bytes": d8.kv_bytes,
+                                         # against this run's bf16 C2 step (only the decode workload has one)
+                                         "speedup_vs_bf16_kv": ((ms / args.steps) / t8
+                                                                if args.workload == "decode" else None),
                                          "variant": p8.config}
             del d8, p8, g8
         except Exception as ex:  # pragma: no cover

@@ -159,6 +159,22 @@ int b200attn_cache_append_fp8(const void* new_k, const void* new_v, void* k_cach
                               int32_t head_dim, int32_t block_size, int32_t num_blocks, float k_scale, float v_scale,
                               void* stream);
 
+/* One serving decode step's host inputs in ONE kernel (attention.DecodeStep; replaces an H2D copy node
+ * + b200attn_cache_append[_fp8]): the SMs read pinned, device-mapped host memory over PCIe and
+ *   - copy copy_bytes (16-byte aligned, multiple of 16) from src to dst (the step's q and seq_lens);
+ *   - append new_k/new_v [num_tokens, kv_heads, 128] bf16 at slot_mapping[num_tokens] into the paged
+ *     cache (bf16, or e4m3 quantised as satfinite_rn(x / k_scale) when kv_dtype = B200ATTN_KV_FP8_E4M3).
+ * Host pointers must be the device-side addresses of pinned memory (b200attn_mapped_ptr). The reference
+ * has no counterpart: its runner feeds device tensors (ref/pkg/runner/src/ktune_triton_runner/backends.py:164). */
+int b200attn_decode_ingest(const void* src, void* dst, int64_t copy_bytes, const void* new_k, const void* new_v,
+                           const int64_t* slot_mapping, void* k_cache, void* v_cache, int32_t num_tokens,
+                           int32_t num_kv_heads, int32_t head_dim, int32_t block_size, int32_t num_blocks,
+                           int32_t kv_dtype, float k_scale, float v_scale, void* stream);
+
+/* Device-side address of pinned (cudaHostAlloc'd / registered) host memory; BAD_ARGS for any other pointer.
+ * Lets the decode kernels write their output straight into a pinned host buffer (zero-copy D2H). */
+int b200attn_mapped_ptr(const void* host, void** dev);
+
 /* Descriptor self-test of the tcgen05 path (one CTA, no TMA):
  *   mode 0: D[128x128]  = A[128x128] . B[128x128]^T   A, B K-major
  *   mode 1: D[128x128]  = A[128x128] . B[128x128]     B MN-major ([K][N] row-major)

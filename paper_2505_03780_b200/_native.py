@@ -75,6 +75,7 @@ EXPORTS = (
     "b200attn_decode_partial",
     "b200attn_combine",
     "b200attn_cache_append", "b200attn_cache_append_fp8", "b200attn_selftest_umma",
+    "b200attn_decode_ingest", "b200attn_mapped_ptr",
 )
 
 _lib = None
@@ -112,10 +113,14 @@ def load():
     lib.b200attn_cache_append_fp8.argtypes = [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, ctypes.c_float,
                                               ctypes.c_float, _P]
     lib.b200attn_selftest_umma.argtypes = [ctypes.c_int, _P, _P, _P, _P]
+    lib.b200attn_decode_ingest.argtypes = [_P, _P, ctypes.c_int64, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I,
+                                           ctypes.c_float, ctypes.c_float, _P]
+    lib.b200attn_mapped_ptr.argtypes = [_P, ctypes.POINTER(ctypes.c_void_p)]
     for name in ("b200attn_prefill_supported", "b200attn_decode_supported", "b200attn_prefill", "b200attn_decode",
                  "b200attn_decode_partial",
                  "b200attn_combine", "b200attn_cache_append", "b200attn_cache_append_fp8", "b200attn_selftest_umma",
-                 "b200attn_decode_num_splits", "b200attn_decode_launches"):
+                 "b200attn_decode_num_splits", "b200attn_decode_launches", "b200attn_decode_ingest",
+                 "b200attn_mapped_ptr"):
         getattr(lib, name).restype = ctypes.c_int
     if lib.b200attn_abi_version() != ABI_VERSION:
         raise RuntimeError(f"libb200attn ABI {lib.b200attn_abi_version()} != {ABI_VERSION}; rebuild the library")

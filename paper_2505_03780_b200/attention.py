@@ -14,6 +14,7 @@ memory and the current CUDA stream.
 
 from __future__ import annotations
 
+import ctypes
 import itertools
 import math
 from typing import Mapping, Optional
@@ -451,6 +452,12 @@ class DecodeStep:
         H2D (pinned staging: q, the new token's K/V, slot_mapping, seq_lens)
         -> cache_append (new K/V into its page slot) -> paged_decode -> D2H (output, pinned)
 
+    With one chunk (the default) the step is three kernels and no copy nodes (``zero_copy``): one
+    ingest kernel reads q, seq_lens and the new K/V straight from the pinned staging buffer over
+    PCIe (device-mapped host memory), copying q/seq_lens to HBM and appending K/V into the pages in
+    the same launch, then K2' + K3' run and write the output rows straight into the pinned
+    ``out_host`` — the copy-engine nodes, their graph edges and the separate append launch are gone.
+
     The batch is cut into ``chunks`` contiguous groups of sequences whose transfers overlap the
     other groups' kernels on separate copy streams: H2D(i+1) runs under decode(i) and D2H(i) under
     decode(i+1), so only the first group's inputs and the last group's output sit on the critical
@@ -463,7 +470,7 @@ class DecodeStep:
     device: a serving loop appends one page index per sequence every ``block_size`` steps, in place."""
 
     def __init__(self, k_cache, v_cache, block_table, batch: int, num_q_heads: int, max_seq_len=None, config=None,
-                 softmax_scale=None, k_scale=None, v_scale=None, chunks: int = 0):
+                 softmax_scale=None, k_scale=None, v_scale=None, chunks: int = 0, zero_copy: bool = True):
         dev = k_cache.device
         _check_cache(k_cache, "k_cache")
         Hkv, D = k_cache.shape[2], k_cache.shape[3]
@@ -476,14 +483,20 @@ class DecodeStep:
         bounds = [B * i // chunks for i in range(chunks + 1)]
         self.bounds = bounds
         self.chunks = chunks
-        # chunk-major pinned staging: chunk i = [q | new_k | new_v | slots | seq_lens] of its rows
+        # chunk-major pinned staging: chunk i = [q | seq_lens | new_k | new_v | slots] of its rows (q and
+        # seq_lens first: the one range the decode kernels read from HBM); views in the order
+        # (q, new_k, new_v, slots, seq_lens)
         protos, self._views = [], []
         for i in range(chunks):
             n = bounds[i + 1] - bounds[i]
-            protos += [torch.empty(n, Hq, D, dtype=torch.bfloat16), torch.empty(n, Hkv, D, dtype=torch.bfloat16),
-                       torch.empty(n, Hkv, D, dtype=torch.bfloat16), torch.full((n,), -1, dtype=torch.int64),
-                       torch.zeros(n, dtype=torch.int32)]
-        self.stage_h, views = pack_pinned(protos)
+            protos += [torch.empty(n, Hq, D, dtype=torch.bfloat16), torch.zeros(n, dtype=torch.int32),
+                       torch.empty(n, Hkv, D, dtype=torch.bfloat16), torch.empty(n, Hkv, D, dtype=torch.bfloat16),
+                       torch.full((n,), -1, dtype=torch.int64)]
+        self.stage_h, packed = pack_pinned(protos)
+        views = []
+        for i in range(chunks):
+            q_, sl_, k_, v_, s_ = packed[5 * i:5 * i + 5]
+            views += [q_, k_, v_, s_, sl_]
         self.stage_d = torch.empty_like(self.stage_h, device=dev)
         self.out_host = torch.empty(B, Hq, D, dtype=torch.bfloat16).pin_memory()
         self.out_d = torch.empty(B, Hq, D, dtype=torch.bfloat16, device=dev)
@@ -495,18 +508,44 @@ class DecodeStep:
             hv = [unpack_view(self.stage_h, v) for v in views[5 * i:5 * i + 5]]
             dv = [unpack_view(self.stage_d, v) for v in views[5 * i:5 * i + 5]]
             self._views.append(hv)
-            lo = views[5 * i][0]
-            last = views[5 * i + 4]
-            hi = last[0] + math.prod(last[1]) * 4
+            lo = packed[5 * i][0]
+            last = packed[5 * i + 4]
+            hi = last[0] + math.prod(last[1]) * 8  # slots (int64) end the chunk
             ranges.append((lo, hi))
             b0, b1 = bounds[i], bounds[i + 1]
             self.plans.append((DecodePlan(dv[0], k_cache, v_cache, block_table[b0:b1], dv[4], out=self.out_d[b0:b1],
                                           max_seq_len=max_seq_len, config=config, softmax_scale=softmax_scale,
                                           k_scale=k_scale, v_scale=v_scale), dv))
         self.config = self.plans[0][0].config
+        self.zero_copy = bool(zero_copy) and chunks == 1
+        if self.zero_copy:
+            lib = _native.load()
+
+            def mapped(t):
+                ptr = ctypes.c_void_p()
+                _native.check(lib.b200attn_mapped_ptr(t.data_ptr(), ctypes.byref(ptr)))
+                return ptr.value
+
+            plan, dv = self.plans[0]
+            plan.p.o = mapped(self.out_host)  # K2' / K3' store the output rows into pinned host memory
+            plan._tensors += (self.out_host,)
+            sl = packed[1]
+            copy_bytes = (sl[0] + math.prod(sl[1]) * 4 + 15) // 16 * 16  # q + seq_lens
+            base = mapped(self.stage_h)
+            off = {name: packed[j][0] for j, name in ((2, "k"), (3, "v"), (4, "s"))}
+            kv_fp8 = _kv_dtype_code(k_cache) == _native.KV_FP8_E4M3
+            self._ingest = (base, self.stage_d.data_ptr(), copy_bytes, base + off["k"], base + off["v"],
+                            base + off["s"], k_cache.data_ptr(), v_cache.data_ptr(), B, Hkv, D, k_cache.shape[1],
+                            k_cache.shape[0], _native.KV_FP8_E4M3 if kv_fp8 else _native.KV_BF16,
+                            float(k_scale or 1.0) if kv_fp8 else 1.0, float(v_scale or 1.0) if kv_fp8 else 1.0)
+            self._kv = (k_cache, v_cache)
 
         def body():
             main = torch.cuda.current_stream(dev)
+            if self.zero_copy:  # ingest kernel (PCIe reads) -> K2' [+ K3'] (output rows written to host)
+                _native.check(_native.load().b200attn_decode_ingest(*self._ingest, main.cuda_stream))
+                self.plans[0][0].run()
+                return
             if chunks == 1:  # one stream: H2D -> append -> decode -> D2H, no cross-stream edges
                 lo, hi = ranges[0]
                 plan, dv = self.plans[0]

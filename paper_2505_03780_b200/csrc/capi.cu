@@ -923,6 +923,51 @@ int b200attn_cache_append_fp8(const void* new_k, const void* new_v, void* k_cach
   return e == cudaSuccess ? B200ATTN_OK : cuda_fail(e, "cache_append_fp8 launch");
 }
 
+int b200attn_mapped_ptr(const void* host, void** dev) {
+  g_err[0] = 0;
+  if (!host || !dev) return fail(B200ATTN_BAD_ARGS, "mapped_ptr args");
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, host);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaPointerGetAttributes");
+  if (at.type != cudaMemoryTypeHost || at.devicePointer == nullptr)
+    return fail(B200ATTN_BAD_ARGS, "pointer %p is not pinned, device-mapped host memory", host);
+  *dev = at.devicePointer;
+  return B200ATTN_OK;
+}
+
+int b200attn_decode_ingest(const void* src, void* dst, int64_t copy_bytes, const void* new_k, const void* new_v,
+                           const int64_t* slot_mapping, void* k_cache, void* v_cache, int32_t num_tokens,
+                           int32_t num_kv_heads, int32_t head_dim, int32_t block_size, int32_t num_blocks,
+                           int32_t kv_dtype, float k_scale, float v_scale, void* stream) {
+  NvtxRange nvtx("b200attn_decode_ingest");
+  g_err[0] = 0;
+  if (head_dim != 128) return fail(B200ATTN_UNSUPPORTED_CONFIG, "head_dim=%d (compiled for 128)", head_dim);
+  if (copy_bytes < 0 || (copy_bytes & 15) || (copy_bytes && (!src || !dst)) ||
+      (reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15))
+    return fail(B200ATTN_BAD_ARGS, "decode_ingest: copy range must be 16-byte aligned (%lld B)", (long long)copy_bytes);
+  if (num_tokens < 0 || num_kv_heads <= 0 || (num_tokens && (!new_k || !new_v || !k_cache || !v_cache || !slot_mapping)))
+    return fail(B200ATTN_BAD_ARGS, "decode_ingest append args");
+  if (kv_dtype != B200ATTN_KV_BF16 && kv_dtype != B200ATTN_KV_FP8_E4M3)
+    return fail(B200ATTN_BAD_ARGS, "decode_ingest: kv_dtype %d", kv_dtype);
+  const bool fp8 = kv_dtype == B200ATTN_KV_FP8_E4M3;
+  if (fp8 && (!(k_scale > 0.f) || !(v_scale > 0.f))) return fail(B200ATTN_BAD_ARGS, "k_scale / v_scale must be > 0");
+  const int threads = 256;
+  const long long n16 = copy_bytes / 16;
+  // enough copy threads for every 16-B load of a C2-sized step (512 KB) to be in flight at once
+  const int copy_blocks = (int)std::min<long long>((n16 + threads - 1) / threads, 2LL * num_sms());
+  const long long rows = (long long)num_tokens * num_kv_heads;
+  const long long append_blocks = (rows * (fp8 ? 16 : 32) + threads - 1) / threads;
+  const long long blocks = copy_blocks + append_blocks;
+  if (blocks == 0) return B200ATTN_OK;
+  b200::decode_ingest_kernel<<<(unsigned)blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), n16, copy_blocks,
+      reinterpret_cast<const uint4*>(new_k), reinterpret_cast<const uint4*>(new_v), k_cache, v_cache, slot_mapping,
+      num_tokens, num_kv_heads, (int64_t)num_blocks * block_size, fp8 ? 1 : 0, fp8 ? 1.f / k_scale : 1.f,
+      fp8 ? 1.f / v_scale : 1.f);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? B200ATTN_OK : cuda_fail(e, "decode_ingest launch");
+}
+
 #ifdef B200_TRACE
 int b200attn_debug_trace(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, b200::g_trace, sizeof(unsigned long long) * (size_t)n);

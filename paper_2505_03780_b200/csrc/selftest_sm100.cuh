@@ -104,20 +104,26 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(const __nv_bfloat16*
 }
 
 // Paged KV-cache append: one warp per (token, kv head), 16-B vectors (128 x bf16 = 256 B row).
-__global__ void cache_append_kernel(const uint4* __restrict__ nk, const uint4* __restrict__ nv,
-                                    uint4* __restrict__ kc, uint4* __restrict__ vc,
-                                    const int64_t* __restrict__ slots, int num_tokens, int kv_heads,
-                                    int64_t num_slots) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= num_tokens * kv_heads) return;
-  const int tok = w / kv_heads, h = w % kv_heads;
+__device__ __forceinline__ void append_row_bf16(long long w, int lane, const uint4* __restrict__ nk,
+                                                const uint4* __restrict__ nv, uint4* __restrict__ kc,
+                                                uint4* __restrict__ vc, const int64_t* __restrict__ slots,
+                                                int num_tokens, int kv_heads, int64_t num_slots) {
+  if (w >= static_cast<long long>(num_tokens) * kv_heads) return;
+  const int tok = static_cast<int>(w / kv_heads), h = static_cast<int>(w % kv_heads);
   const int64_t slot = slots[tok];
   if (slot < 0 || slot >= num_slots) return;
   const int64_t src = (static_cast<int64_t>(tok) * kv_heads + h) * 16;  // 16 uint4 per 128-wide row
   const int64_t dst = (slot * kv_heads + h) * 16;
   if (lane < 16) kc[dst + lane] = nk[src + lane];
   else vc[dst + lane - 16] = nv[src + lane - 16];
+}
+
+__global__ void cache_append_kernel(const uint4* __restrict__ nk, const uint4* __restrict__ nv,
+                                    uint4* __restrict__ kc, uint4* __restrict__ vc,
+                                    const int64_t* __restrict__ slots, int num_tokens, int kv_heads,
+                                    int64_t num_slots) {
+  append_row_bf16((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5, threadIdx.x & 31, nk, nv,
+                  kc, vc, slots, num_tokens, kv_heads, num_slots);
 }
 
 // fp8 variant: 16 lanes per (token, kv head) row, 8 bf16 -> 8 e4m3 each (satfinite, RN), K and V.
@@ -134,12 +140,11 @@ __device__ __forceinline__ uint2 bf16x8_to_e4m3x8(uint4 x, float inv) {
                     f32x4_to_e4m3x4(f(x.z, 0), f(x.z, 1), f(x.w, 0), f(x.w, 1)));
 }
 
-__global__ void cache_append_fp8_kernel(const uint4* __restrict__ nk, const uint4* __restrict__ nv,
-                                        uint2* __restrict__ kc, uint2* __restrict__ vc,
-                                        const int64_t* __restrict__ slots, int num_tokens, int kv_heads,
-                                        int64_t num_slots, float inv_k, float inv_v) {
-  const long long g = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 4;
-  const int l = threadIdx.x & 15;
+__device__ __forceinline__ void append_row_fp8(long long g, int l, const uint4* __restrict__ nk,
+                                               const uint4* __restrict__ nv, uint2* __restrict__ kc,
+                                               uint2* __restrict__ vc, const int64_t* __restrict__ slots,
+                                               int num_tokens, int kv_heads, int64_t num_slots, float inv_k,
+                                               float inv_v) {
   if (g >= static_cast<long long>(num_tokens) * kv_heads) return;
   const int tok = static_cast<int>(g / kv_heads), h = static_cast<int>(g % kv_heads);
   const int64_t slot = slots[tok];
@@ -148,6 +153,49 @@ __global__ void cache_append_fp8_kernel(const uint4* __restrict__ nk, const uint
   const int64_t dst = (slot * kv_heads + h) * 16 + l;                       // 8 fp8 per lane
   kc[dst] = bf16x8_to_e4m3x8(nk[src], inv_k);
   vc[dst] = bf16x8_to_e4m3x8(nv[src], inv_v);
+}
+
+__global__ void cache_append_fp8_kernel(const uint4* __restrict__ nk, const uint4* __restrict__ nv,
+                                        uint2* __restrict__ kc, uint2* __restrict__ vc,
+                                        const int64_t* __restrict__ slots, int num_tokens, int kv_heads,
+                                        int64_t num_slots, float inv_k, float inv_v) {
+  append_row_fp8((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 4, threadIdx.x & 15, nk, nv, kc,
+                 vc, slots, num_tokens, kv_heads, num_slots, inv_k, inv_v);
+}
+
+// One serving decode step's host inputs in ONE kernel (attention.DecodeStep), read by the SMs
+// straight from pinned, device-mapped host memory over PCIe: blocks [0, copy_blocks) copy the
+// step's q and seq_lens (one contiguous staging range, 16-B vectors, 4 loads in flight per thread)
+// into device memory; the remaining blocks append the new token's K/V into its page slot (the
+// cache_append rows above, reading new_k / new_v / slot_mapping from the host).  Replaces an H2D
+// copy node + the append kernel: both are PCIe-latency-bound and now overlap each other.
+__global__ void __launch_bounds__(256) decode_ingest_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                            long long n16, int copy_blocks,
+                                                            const uint4* __restrict__ nk,
+                                                            const uint4* __restrict__ nv, void* kc, void* vc,
+                                                            const int64_t* __restrict__ slots, int num_tokens,
+                                                            int kv_heads, int64_t num_slots, int fp8, float inv_k,
+                                                            float inv_v) {
+  if (static_cast<int>(blockIdx.x) < copy_blocks) {
+    const long long stride = static_cast<long long>(copy_blocks) * blockDim.x;
+    long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n16; i += 4 * stride) {
+      const uint4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
+      dst[i] = a;
+      dst[i + stride] = b;
+      dst[i + 2 * stride] = c;
+      dst[i + 3 * stride] = d;
+    }
+    for (; i < n16; i += stride) dst[i] = src[i];
+    return;
+  }
+  const long long t = static_cast<long long>(blockIdx.x - copy_blocks) * blockDim.x + threadIdx.x;
+  if (fp8)
+    append_row_fp8(t >> 4, threadIdx.x & 15, nk, nv, reinterpret_cast<uint2*>(kc), reinterpret_cast<uint2*>(vc),
+                   slots, num_tokens, kv_heads, num_slots, inv_k, inv_v);
+  else
+    append_row_bf16(t >> 5, threadIdx.x & 31, nk, nv, reinterpret_cast<uint4*>(kc), reinterpret_cast<uint4*>(vc),
+                    slots, num_tokens, kv_heads, num_slots);
 }
 
 // fp8 (e4m3) descriptor self-test: D[128x128] = A . B^T with 128-byte rows.

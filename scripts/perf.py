@@ -322,13 +322,14 @@ def cmd_e2e(a):
         f = (lambda: dd.copy_(h, non_blocking=True)) if name.startswith("h2d") else (lambda: h.copy_(dd, non_blocking=True))
         res[name + "_us"] = ev_time(f)[0]
     slots_h = torch.full((B,), -1, dtype=torch.int64)
-    for chunks in (1, 2, 3, 4, 8):
+    for chunks, zc in ((1, True), (1, False), (2, False), (4, False)):
         step = A.DecodeStep(d.k_cache, d.v_cache, d.block_table, batch=B, num_q_heads=Hq, max_seq_len=d.max_seq_len,
-                            chunks=chunks)
+                            chunks=chunks, zero_copy=zc)
         step.set_inputs(d.q.cpu(), nk.cpu(), nk.cpu(), slots_h, d.seq_lens.cpu())
         dev_us, wall_us = ev_time(step)
-        res[f"step_chunks{chunks}_us"] = dev_us
-        res[f"step_chunks{chunks}_wall_us"] = wall_us
+        tag = f"step_chunks{chunks}" + ("_zerocopy" if zc else "")
+        res[f"{tag}_us"] = dev_us
+        res[f"{tag}_wall_us"] = wall_us
         del step
     print(json.dumps({"tag": a.tag, **{k: round(v, 2) for k, v in res.items()}}), flush=True)
 

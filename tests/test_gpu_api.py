@@ -73,8 +73,8 @@ def test_two_streams_in_flight_do_not_share_workspace():
             assert torch.equal(outs_d[i], ref_d[i])
 
 
-@pytest.mark.parametrize("chunks", [1, 2, 3])
-def test_decode_step_graph_matches_eager_api(chunks):
+@pytest.mark.parametrize("chunks,zero_copy", [(1, True), (1, False), (2, False), (3, False)])
+def test_decode_step_graph_matches_eager_api(chunks, zero_copy):
     """DecodeStep (H2D -> cache_append -> paged_decode -> D2H in one CUDA graph, the batch in
     chunks overlapping copies and kernels): the cache pages it writes equal the eager cache_append's
     bit for bit, its output matches the oracle, and with one chunk it equals the eager paged_decode
@@ -83,8 +83,9 @@ def test_decode_step_graph_matches_eager_api(chunks):
     B = len(lens)
     d = W.make_decode(dict(W.C2, batch_size=B, seq_len=4096), device=DEV, lens=lens, extra_blocks=2)
     k2, v2 = d.k_cache.clone(), d.v_cache.clone()
-    step = A.DecodeStep(d.k_cache, d.v_cache, d.block_table, batch=B, num_q_heads=32, chunks=chunks)
-    assert step.chunks == chunks
+    step = A.DecodeStep(d.k_cache, d.v_cache, d.block_table, batch=B, num_q_heads=32, chunks=chunks,
+                        zero_copy=zero_copy)
+    assert step.chunks == chunks and step.zero_copy == zero_copy
     g = torch.Generator().manual_seed(1)
     bs = 16
     bt = d.block_table.cpu()
@@ -102,6 +103,52 @@ def test_decode_step_graph_matches_eager_api(chunks):
         if chunks == 1:  # same sequences per launch as the eager call: bit-identical
             ref = A.paged_decode(q.to(DEV), k2, v2, d.block_table, d.seq_lens)
             assert torch.equal(out, ref.cpu())
+
+
+def test_decode_step_zero_copy_fp8_cache():
+    """The zero-copy DecodeStep over an e4m3 cache: its ingest kernel quantises the new K/V into the
+    pages bit for bit like the eager cache_append_fp8, and the output (written by K2'/K3' straight
+    into pinned host memory) equals the eager paged_decode's bit for bit and the fp8 oracle."""
+    lens = [300, 5, 64, 2000, 17]
+    B = len(lens)
+    d = W.make_decode(dict(W.C2, batch_size=B, seq_len=2048, kv_dtype="fp8_e4m3"), device=DEV, lens=lens,
+                      extra_blocks=2)
+    k2, v2 = d.k_cache.clone(), d.v_cache.clone()
+    step = A.DecodeStep(d.k_cache, d.v_cache, d.block_table, batch=B, num_q_heads=32, k_scale=d.k_scale,
+                        v_scale=d.v_scale)
+    assert step.zero_copy
+    g = torch.Generator().manual_seed(3)
+    bs = 16
+    bt = d.block_table.cpu()
+    for it in range(2):
+        q = torch.randn(B, 32, 128, generator=g).bfloat16()
+        nk, nv = (torch.randn(B, 8, 128, generator=g).bfloat16() for _ in range(2))
+        slots = torch.tensor([int(bt[b, (n - 1) // bs]) * bs + (n - 1) % bs for b, n in enumerate(lens)])
+        step.set_inputs(q, nk, nv, slots, torch.tensor(lens, dtype=torch.int32))
+        out = step(sync=True).clone()
+        A.cache_append(nk.to(DEV), nv.to(DEV), k2, v2, slots.to(DEV), k_scale=d.k_scale, v_scale=d.v_scale)
+        torch.cuda.synchronize()
+        assert torch.equal(d.k_cache.view(torch.uint8), k2.view(torch.uint8))
+        assert torch.equal(d.v_cache.view(torch.uint8), v2.view(torch.uint8))
+        ref = A.paged_decode(q.to(DEV), k2, v2, d.block_table, d.seq_lens, k_scale=d.k_scale, v_scale=d.v_scale)
+        assert torch.equal(out, ref.cpu())
+        o = oracle.decode_fp8_np(q, k2.cpu(), v2.cpu(), bt, torch.tensor(lens, dtype=torch.int32), d.k_scale,
+                                 d.v_scale)
+        assert np.abs(out.float().numpy() - o).max() < 1e-2
+
+
+def test_mapped_ptr_rejects_device_and_pageable_memory():
+    """b200attn_mapped_ptr (the zero-copy output / ingest addresses) accepts pinned host memory only."""
+    import ctypes
+
+    from paper_2505_03780_b200 import _native
+
+    lib = _native.load()
+    out = ctypes.c_void_p()
+    pinned = torch.empty(1024, dtype=torch.uint8).pin_memory()
+    assert lib.b200attn_mapped_ptr(pinned.data_ptr(), ctypes.byref(out)) == 0 and out.value
+    for t in (torch.empty(1024, dtype=torch.uint8, device=DEV), torch.empty(1024, dtype=torch.uint8)):
+        assert lib.b200attn_mapped_ptr(t.data_ptr(), ctypes.byref(out)) == _native.BAD_ARGS
 
 
 @pytest.mark.parametrize("chunks", [1, 3])
