@@ -583,15 +583,20 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
   cudaError_t e = launch_k(kern, dim3(ctas), dim3(C::NTHREADS), smem, stream, mq, mk, mv, a);
   if (e != cudaSuccess) return cuda_fail(e, "decode_flat launch");
   if (combine && !fused) {
+    // (warps, pieces in flight per warp) sized so the grid stays one wave (see flat_combine_kernel)
+    const long long cg = (long long)p->batch * C::NQ;
+    auto ck = cg <= num_sms()       ? b200::flat_combine_kernel<C::NQ, 8, 8, 1>
+              : cg <= 4LL * num_sms() ? b200::flat_combine_kernel<C::NQ, 8, 4, 4>
+                                      : b200::flat_combine_kernel<C::NQ, 4, 1, 16>;
+    const dim3 cgrid(p->batch, C::NQ), cblock(cg <= 4LL * num_sms() ? 256 : 128);
     if (pdl_combine) {  // K2' triggers late, so K3' becomes resident only in K2's tail
-      e = launch_k(b200::flat_combine_kernel<C::NQ>, dim3(p->batch, C::NQ), dim3(128), 0, stream,
-                   (const float*)a.part_o, (const float*)a.part_ml, (const int32_t*)a.cu_tiles_out, (int)p->batch,
-                   ctas, reinterpret_cast<__nv_bfloat16*>(p->o));
+      e = launch_k(ck, cgrid, cblock, 0, stream, (const float*)a.part_o, (const float*)a.part_ml,
+                   (const int32_t*)a.cu_tiles_out, (int)p->batch, ctas, reinterpret_cast<__nv_bfloat16*>(p->o));
     } else {
       // a plain launch: PDL-launched while K2' triggered at its start, its CTAs sat resident beside
       // K2' and the 1-sequence x 8k decode lost 6 us (22.1 vs 15.9 us, r2d pdlab)
-      b200::flat_combine_kernel<C::NQ><<<dim3(p->batch, C::NQ), 128, 0, stream>>>(
-          a.part_o, a.part_ml, a.cu_tiles_out, p->batch, ctas, reinterpret_cast<__nv_bfloat16*>(p->o));
+      ck<<<cgrid, cblock, 0, stream>>>(a.part_o, a.part_ml, a.cu_tiles_out, p->batch, ctas,
+                                       reinterpret_cast<__nv_bfloat16*>(p->o));
       e = cudaGetLastError();
     }
     if (e != cudaSuccess) return cuda_fail(e, "flat combine launch");

@@ -762,99 +762,96 @@ __global__ void __launch_bounds__(FlatCfg<HKV, G, NSTAGE, FP8>::NTHREADS, 1)
 }
 
 // K3': merge the partial segments of every split sequence (sequences finished inside one CTA
-// were already written by it).  One CTA per (sequence, q head); the up-to-148 partials of a
-// sequence are reduced in parallel — max and weights across threads, then each warp sums a
-// quarter of the partial rows with float4 loads (4 in flight per lane) — instead of one
-// dependent load chain per partial (which made a 1-sequence decode latency-bound at ~100 us).
+// were already written by it).
+// One CTA per (sequence, q head).  Single pass: every warp folds its share of the pieces (piece i
+// to warp i mod NW, U pieces' (max, sum) pairs and 512-byte O rows loaded back to back before any
+// is folded) into a running (m, l, acc) with the online-softmax rescale, then warp 0 folds the NW
+// warp states in warp order — deterministic, so launches are bit-identical.  One dependent L2 round
+// trip per U * NW pieces (the earlier max pass -> weights -> rows chain took 3 + nc / 16).  The
+// launcher keeps the grid in one wave: (NW, U) = (8, 8) up to one CTA per SM (a 1-sequence x 8k
+// decode: 128 pieces per head in 2 rounds), (8, 4) at 4 CTAs per SM, else (4, 1) at 16 CTAs per SM
+// (C2's 2048 CTAs; 76 registers at U = 8 had made that two waves, +1.3 us on the step).
 constexpr int kFlatMaxCtas = 1024;
-
-template <int NQ>
-__global__ void __launch_bounds__(128) flat_combine_kernel(const float* __restrict__ part_o,
-                                                           const float* __restrict__ part_ml,
-                                                           const int32_t* __restrict__ cu, int batch, int ctas,
-                                                           __nv_bfloat16* __restrict__ o) {
-  __shared__ float sw[kFlatMaxCtas];
-  __shared__ float red[4];
-  __shared__ float4 acc_s[4][32];
+template <int NQ, int NW, int U, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) flat_combine_kernel(const float* __restrict__ part_o,
+                                                                     const float* __restrict__ part_ml,
+                                                                     const int32_t* __restrict__ cu, int batch,
+                                                                     int ctas, __nv_bfloat16* __restrict__ o) {
+  __shared__ float ml_w[NW][2];
+  __shared__ float4 acc_w[NW][32];
+  __shared__ uint8_t own_s[kFlatMaxCtas];
   const int b = blockIdx.x, q = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   griddep_wait();  // PDL: K2' (the predecessor) has completed and its partials are visible
   griddep_launch();
   const int ts = cu[b], te = cu[b + 1], n = cu[batch];
   __nv_bfloat16* out = o + (static_cast<size_t>(b) * NQ + q) * 128;
   if (ts == te) {
-    out[tid] = __float2bfloat16_rn(0.f);
+    if (tid < 64) reinterpret_cast<uint32_t*>(out)[tid] = 0u;
     return;
   }
   const int c0 = flat_cta_of(ts, ctas, n), c1 = flat_cta_of(te - 1, ctas, n);
-  if (c0 == c1) return;
+  if (c0 == c1) return;  // K2' wrote this sequence's output itself
   const int nc = c1 - c0 + 1;
-  // CTAs whose range is empty (fewer tiles than CTAs) wrote nothing: skip their slots
-  auto owns = [&](int c) {
-    return static_cast<long long>(c) * n / ctas != (static_cast<long long>(c) + 1) * n / ctas;
-  };
-  auto ml = [&](int c, int k) { return part_ml[((static_cast<size_t>(c) + b) * NQ + q) * 2 + k]; };
-  float m = -INFINITY;
-  for (int i = tid; i < nc; i += 128)
-    if (owns(c0 + i)) m = fmaxf(m, ml(c0 + i, 0));
-#pragma unroll
-  for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-  if (lane == 0) red[warp] = m;
-  __syncthreads();
-  const float M = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-  __syncthreads();
-  float l = 0.f;
-  for (int i = tid; i < nc; i += 128) {
-    const int c = c0 + i;
-    const float w = owns(c) ? fast_exp2(ml(c, 0) - M) : 0.f;
-    sw[i] = w;
-    if (w != 0.f) l = fmaf(w, ml(c, 1), l);
+  // CTAs whose range is empty (fewer tiles than CTAs) wrote nothing: their slots are skipped
+  // (flags computed once, one piece per thread, off the load chain)
+  for (int i = tid; i < nc; i += NW * 32) {
+    const long long c = c0 + i;
+    own_s[i] = (c * n / ctas != (c + 1) * n / ctas) ? 1 : 0;
   }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-  if (lane == 0) red[warp] = l;
   __syncthreads();
-  const float L = red[0] + red[1] + red[2] + red[3];
+  float m = -INFINITY, l = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  auto row = [&](int i) {
-    return reinterpret_cast<const float4*>(part_o + ((static_cast<size_t>(c0 + i) + b) * NQ + q) * 128) + lane;
-  };
-  int i = warp;
-  for (; i + 12 < nc; i += 16) {  // 4 partial rows per warp per round, loads issued back to back
-    float4 v[4];
-    float w[4];
+  for (int i0 = warp; i0 < nc; i0 += NW * U) {
+    float mp[U], lp[U];
+    float4 v[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      w[u] = sw[i + 4 * u];
-      v[u] = w[u] != 0.f ? __ldg(row(i + 4 * u)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * NW;
+      mp[u] = -INFINITY;
+      lp[u] = 0.f;
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < nc && own_s[i]) {
+        const size_t slot = (static_cast<size_t>(c0 + i) + b) * NQ + q;
+        mp[u] = __ldcg(part_ml + slot * 2);
+        lp[u] = __ldcg(part_ml + slot * 2 + 1);
+        v[u] = __ldcg(reinterpret_cast<const float4*>(part_o + slot * 128) + lane);
+      }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      acc.x = fmaf(w[u], v[u].x, acc.x);
-      acc.y = fmaf(w[u], v[u].y, acc.y);
-      acc.z = fmaf(w[u], v[u].z, acc.z);
-      acc.w = fmaf(w[u], v[u].w, acc.w);
+    for (int u = 0; u < U; ++u) {
+      const float mn = fmaxf(m, mp[u]);
+      if (mn == -INFINITY) continue;
+      const float wa = fast_exp2(m - mn), wb = fast_exp2(mp[u] - mn);
+      l = fmaf(l, wa, lp[u] * wb);
+      acc.x = fmaf(acc.x, wa, v[u].x * wb);
+      acc.y = fmaf(acc.y, wa, v[u].y * wb);
+      acc.z = fmaf(acc.z, wa, v[u].z * wb);
+      acc.w = fmaf(acc.w, wa, v[u].w * wb);
+      m = mn;
     }
   }
-  for (; i < nc; i += 4) {
-    const float w = sw[i];
-    if (w != 0.f) {
-      const float4 v = __ldg(row(i));
-      acc.x = fmaf(w, v.x, acc.x);
-      acc.y = fmaf(w, v.y, acc.y);
-      acc.z = fmaf(w, v.z, acc.z);
-      acc.w = fmaf(w, v.w, acc.w);
-    }
+  if (lane == 0) {
+    ml_w[warp][0] = m;
+    ml_w[warp][1] = l;
   }
-  acc_s[warp][lane] = acc;
+  acc_w[warp][lane] = acc;
   __syncthreads();
   if (warp == 0) {
-    float4 r = acc_s[0][lane];
+    float M = -INFINITY;
 #pragma unroll
-    for (int k = 1; k < 4; ++k) {
-      r.x += acc_s[k][lane].x;
-      r.y += acc_s[k][lane].y;
-      r.z += acc_s[k][lane].z;
-      r.w += acc_s[k][lane].w;
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, ml_w[w][0]);
+    float L = 0.f;
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      if (ml_w[w][0] == -INFINITY) continue;
+      const float s = fast_exp2(ml_w[w][0] - M);
+      const float4 a = acc_w[w][lane];
+      L = fmaf(ml_w[w][1], s, L);
+      r.x = fmaf(a.x, s, r.x);
+      r.y = fmaf(a.y, s, r.y);
+      r.z = fmaf(a.z, s, r.z);
+      r.w = fmaf(a.w, s, r.w);
     }
     const float inv = L > 0.f ? 1.f / L : 0.f;
     __nv_bfloat162 lo = __floats2bfloat162_rn(r.x * inv, r.y * inv), hi = __floats2bfloat162_rn(r.z * inv, r.w * inv);

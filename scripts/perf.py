@@ -269,13 +269,13 @@ def cmd_dtrace(a):
         for _ in range(5):
             p.run()
         torch.cuda.synchronize()
-        buf = (ctypes.c_ulonglong * (1024 * 9))()
-        lib.b200attn_debug_dtrace(buf, 1024 * 9)
-        t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 9).astype(np.int64)
+        buf = (ctypes.c_ulonglong * (1024 * 8))()
+        rc = lib.b200attn_debug_dtrace(buf, 1024 * 8)  # [1024 CTAs][8 events]
+        assert rc == 0, f"b200attn_debug_dtrace: cuda error {rc} (is B200ATTN_LIB the trace build?)"
+        t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8).astype(np.int64)
         n = int(p.num_splits) if p.config.get("TILE_N") == 16 else 0
         t = t[:n] if n else t[:148]
-        smid = t[:, 8].copy()
-        t = t[:, :8]
+        smid = np.full(len(t), -1)
         t0 = t[:, 0][t[:, 0] > 0].min()
         rel = (t - t0) / 1e3  # us
         out = {"tag": a.tag, "shape": name, "cfg": p.config, "ctas": int(len(t))}
