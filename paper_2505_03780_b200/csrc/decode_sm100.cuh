@@ -370,24 +370,39 @@ __global__ void __launch_bounds__(DecodeCfg<NSTAGE>::NTHREADS)
   }
 }
 
-// K3: O[b,h,:] = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s   (m in log2 units)
+// K3: O[b,h,:] = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s   (m in log2 units).
+// One pass: the splits' (max, sum) pairs and O values are loaded 8 at a time, back to back, and
+// folded into a running (m, l, acc) with the online-softmax rescale — one dependent L2 round trip
+// per 8 splits instead of a max pass followed by a weighted-sum pass.
 __global__ void __launch_bounds__(128) decode_combine_kernel(const float* __restrict__ part_o,
                                                               const float* __restrict__ part_ml,
                                                               __nv_bfloat16* __restrict__ o, int num_splits) {
+  constexpr int U = 8;
   const int row = blockIdx.x;  // b * Hq + h
   const int d = threadIdx.x;
   const float* ml = part_ml + static_cast<size_t>(row) * num_splits * 2;
-  float M = -INFINITY;
-  for (int s = 0; s < num_splits; ++s) M = fmaxf(M, ml[2 * s]);
-  float acc = 0.f, L = 0.f;
-  if (M != -INFINITY) {
-    for (int s = 0; s < num_splits; ++s) {
-      const float w = fast_exp2(ml[2 * s] - M);
-      L = fmaf(w, ml[2 * s + 1], L);
-      acc = fmaf(w, part_o[(static_cast<size_t>(row) * num_splits + s) * 128 + d], acc);
+  const float* po = part_o + static_cast<size_t>(row) * num_splits * 128 + d;
+  float m = -INFINITY, l = 0.f, acc = 0.f;
+  for (int s0 = 0; s0 < num_splits; s0 += U) {
+    float mp[U], lp[U], op[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = s0 + u < num_splits;
+      mp[u] = ok ? __ldcg(ml + 2 * (s0 + u)) : -INFINITY;
+      lp[u] = ok ? __ldcg(ml + 2 * (s0 + u) + 1) : 0.f;
+      op[u] = ok ? __ldcg(po + static_cast<size_t>(s0 + u) * 128) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float mn = fmaxf(m, mp[u]);
+      if (mn == -INFINITY) continue;
+      const float wa = fast_exp2(m - mn), wb = fast_exp2(mp[u] - mn);
+      l = fmaf(l, wa, lp[u] * wb);
+      acc = fmaf(acc, wa, op[u] * wb);
+      m = mn;
     }
   }
-  o[static_cast<size_t>(row) * 128 + d] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+  o[static_cast<size_t>(row) * 128 + d] = __float2bfloat16_rn(l > 0.f ? acc / l : 0.f);
 }
 
 }  // namespace b200
