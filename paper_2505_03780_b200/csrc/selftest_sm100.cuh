@@ -176,6 +176,10 @@ __global__ void __launch_bounds__(256) decode_ingest_kernel(const uint4* __restr
                                                             const int64_t* __restrict__ slots, int num_tokens,
                                                             int kv_heads, int64_t num_slots, int fp8, float inv_k,
                                                             float inv_v) {
+  // PDL: K2' (launched programmatically behind this kernel) may start its prologue — barrier
+  // init, TMEM alloc, descriptor prefetch — while the PCIe reads are in flight; its
+  // griddepcontrol.wait still orders every data access after this grid's completion
+  griddep_launch();
   if (static_cast<int>(blockIdx.x) < copy_blocks) {
     const long long stride = static_cast<long long>(copy_blocks) * blockDim.x;
     long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
