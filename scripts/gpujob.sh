@@ -21,6 +21,9 @@
 #   umma       tcgen05 MMA issue-rate probe            c5      the C5 sweep (unmodified ktune tune, exhaustive)
 #   pairtests / pairab   CTA-pair K1 parity / A/B      bandtests / bandab   banded K1 order parity / A/B
 #   smalldec / mergesmall   small decode shapes (dispatch vs K2', per-CTA timelines), merge modes
+#   e2eab      perf.py e2e with two builds (base/new)   pdlcombine  K3' PDL behind a late K2' trigger, on/off
+#   smalltime  latency-bound decode shapes: dispatch vs K2' forced      decodetests  the decode/step GPU tests
+#   (decode library A/B: LIBAB_OP=decode LIBAB_SHAPES=d1x8k,C2,... with the libab recipe; K2' timelines: dtrace)
 set -u
 TAG=$1; shift
 mkdir -p gpurun_out
@@ -117,6 +120,22 @@ for r in "$@"; do
                      '{"BLOCK_M": 128, "BLOCK_N": 128, "num_warps": 4, "num_stages": 3, "waves_per_eu": 1, "PRE_LOAD_V": false}'; do
               timeout 300 python scripts/perf.py time --op prefill --shapes C3,1x16k,4x8k,C1 --cfg "$c" --tag "$c"
             done > ${O}_pairab.log 2>&1; cat ${O}_pairab.log ;;
+    e2eab) # DecodeStep e2e breakdown (perf.py e2e) with two library builds alternating (base = _lib/libb200attn_base.so)
+            for rr in 1 2; do for lib in base new; do
+              f=$PWD/paper_2505_03780_b200/_lib/libb200attn.so; [ $lib = base ] && f=$PWD/paper_2505_03780_b200/_lib/libb200attn_base.so
+              B200ATTN_LIB=$f timeout 300 python scripts/perf.py e2e --tag $lib
+            done; done > ${O}_e2eab.log 2>&1; cat ${O}_e2eab.log ;;
+    pdlcombine) for v in 0 1; do B200ATTN_PDL_COMBINE=$v timeout 300 python scripts/perf.py time --tag pdlc$v \
+                  --shapes d1x2k,d1x8k,d4x2k,d16x512,d64x512,C2 --cfg '{"TILE_N": 16, "num_splits": 0, "num_stages": 4}'; done \
+                  > ${O}_pdlcombine.log 2>&1; cat ${O}_pdlcombine.log ;;
+    smalltime) # the C5 grid's latency-bound decode shapes: shipped dispatch vs K2' forced
+            timeout 600 python scripts/perf.py time --tag dispatch \
+              --shapes d1x128,d1x512,d1x2k,d1x8k,d4x512,d4x2k,d16x128,d16x512,d64x512,C2 > ${O}_smalltime.log 2>&1
+            timeout 600 python scripts/perf.py time --tag flat --cfg '{"TILE_N": 16, "num_splits": 0, "num_stages": 4}' \
+              --shapes d1x128,d1x512,d1x2k,d1x8k,d4x512,d4x2k,d16x128,d16x512,d64x512,C2 >> ${O}_smalltime.log 2>&1
+            cat ${O}_smalltime.log ;;
+    decodetests) timeout 900 python -m pytest tests -q -m gpu -k "decode or flat or combine or split or step" \
+                   > ${O}_decodetests.log 2>&1; tail -3 ${O}_decodetests.log ;;
     *) echo "unknown recipe $r" >&2 ;;
   esac
 done
