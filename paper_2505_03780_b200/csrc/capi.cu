@@ -557,6 +557,8 @@ int launch_flat(const b200attn_decode_params* p, bool combine, cudaStream_t stre
     if ((rc = make_map_3d(&mv, p->v_cache, D, tokens, HKV, (uint64_t)HKV * D * 2, D * 2ull, 16, HKV))) return rc;
   }
   const int ctas = flat_ctas(p);
+  if (ctas > b200::kFlatMaxCtas)  // K3' keeps one ownership flag per piece in a kFlatMaxCtas smem array
+    return fail(B200ATTN_UNSUPPORTED_CONFIG, "decode_flat: %d CTAs > %d", ctas, b200::kFlatMaxCtas);
   const size_t slots = (size_t)num_sms() + p->batch;
   b200::FlatDecodeArgs a;
   a.block_table = p->block_table;
