@@ -394,6 +394,30 @@ def test_decode_ragged(lens, cfg):
     check(f"decode {lens} {cfg}", out, ref, base)
 
 
+@pytest.mark.parametrize("lens,hq", [
+    ([8000], 32),                        # 1 x 32 = 32 merge CTAs -> (8 warps, 8 pieces in flight); ~128 pieces
+    ([3000, 1, 700, 2048, 16, 5000], 32),  # 192 merge CTAs -> (8, 4), ragged, a 1-token sequence
+    ([500, 37, 1500, 800] * 10, 16),     # 40 x 16 = 640 merge CTAs -> (4, 1)
+    ([20000, 3], 8),                     # GQA 8/8 (G = 1): 16 merge CTAs, a sequence over every CTA
+], ids=["1x8000", "6ragged", "40x_hq16", "hq8_long"])
+def test_decode_flat_single_pass_merge_shapes(lens, hq):
+    """K3' (single-pass online merge) in each of its three launch shapes — (warps, pieces in flight)
+    = (8, 8) / (8, 4) / (4, 1) picked by the grid size — against the oracle, and bit-identical on a
+    second launch (fixed fold order)."""
+    cfg = dcfg(0, 4, 16)
+    out, ref, base = run_decode(lens, Hq=hq, cfg=cfg)
+    check(f"decode flat K3' shape {len(lens)}x{max(lens)} hq={hq}", out, ref, base)
+    out2, _, _ = run_decode(lens, Hq=hq, cfg=cfg)
+    assert torch.equal(out, out2)
+
+
+@pytest.mark.parametrize("splits", [2, 7, 16])
+def test_decode_split_single_pass_merge(splits):
+    """K3 (split-KV path, single-pass merge over 8 splits per round) at 2 / 7 / 16 splits vs the oracle."""
+    out, ref, base = run_decode([3000, 1, 900, 129], cfg=dcfg(splits, 4, 128))
+    check(f"decode K2 splits={splits}", out, ref, base)
+
+
 @pytest.mark.parametrize("bs", [8, 16, 32, 64, 128])
 @pytest.mark.parametrize("tile", [16, 128])
 def test_decode_block_sizes(bs, tile):
