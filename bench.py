@@ -725,8 +725,8 @@ def run_b200(args, world, rank, local, gpu):
         e2e = {"value": world * units / (e_ms / 1e3) / 1e12, "unit": unit, "h2d_bytes_per_step": step.h2d_bytes,
                "d2h_bytes_per_step": step.d2h_bytes, "ms_per_step": e_ms, "chunks": step.chunks,
                "path": "paper_2505_03780_b200.PrefillStep (public API: one CUDA graph; the varlen batch in groups of "
-                       "sequences whose H2D of q/k/v/cu_seqlens from pinned memory, prefill and D2H of the output "
-                       "overlap across groups on two copy streams)"}
+                       "sequences, heaviest group first, whose H2D of q/k/v/cu_seqlens from pinned memory, prefill and "
+                       "D2H of the output overlap across groups on two copy streams)"}
     del g
 
     # ------------------------------------------------------------------ strong-scaled, validated extras (any N)

@@ -631,9 +631,11 @@ class PrefillStep:
         lens = [int(n) for n in seq_lens]
         T, Hq, Hkv, D = sum(lens), int(num_q_heads), int(num_kv_heads), int(head_dim)
         if chunks <= 0:
-            # the copies dominate (C3: 410 MB in, 274 MB out): 4 groups hide all but ~1/4 of the
-            # last group's read-back and the first group's upload
-            chunks = 4
+            # the copies dominate (C3: 410 MB in, 274 MB out; 7.4 ms of upload at 55 GB/s): with the
+            # heaviest group first, 16 groups leave only the lightest group's prefill + read-back after
+            # the last upload (C3 step: 8.69 ms at 16 groups, 8.93 at 8, 9.73 at 4; 9.52 at 16 in batch
+            # order, whose last group was the 8192-token sequence — perf.py pfe2e, r2p1/r2p2)
+            chunks = 16
         chunks = max(1, min(chunks, len(lens)))
         # group boundaries (sequence indices) at ~equal token counts
         bounds, acc, cut = [0], 0, 1
@@ -673,6 +675,11 @@ class PrefillStep:
             self.plans.append(PrefillPlan(dv[0], dv[1], dv[2], dv[3], max(g), out=self.out_d[tok[i]:tok[i + 1]],
                                           causal=causal, config=config, softmax_scale=softmax_scale))
         self.config = self.plans[0].config
+        # groups run heaviest first (causal work ~ sum L^2): what is left after the last upload is
+        # that group's prefill + read-back, so it should be the lightest one.  In batch order C3's
+        # last group is its 8192-token sequence (~0.5 ms of prefill + 67 MB of read-back).
+        self.order = sorted(range(self.chunks), key=lambda i: -sum(n * n for n in lens[bounds[i]:bounds[i + 1]]))
+        order = self.order
 
         def body():
             main = torch.cuda.current_stream(dev)
@@ -681,15 +688,16 @@ class PrefillStep:
             self._cin.wait_stream(main)
             self._cout.wait_stream(main)
             with torch.cuda.stream(self._cin):
-                for i, (lo, hi) in enumerate(ranges):
+                for i in order:
+                    lo, hi = ranges[i]
                     self.stage_d[lo:hi].copy_(self.stage_h[lo:hi], non_blocking=True)
                     ev_in[i].record()
-            for i, plan in enumerate(self.plans):
+            for i in order:
                 main.wait_event(ev_in[i])
-                plan.run()
+                self.plans[i].run()
                 ev_done[i].record(main)
             with torch.cuda.stream(self._cout):
-                for i in range(self.chunks):
+                for i in order:
                     self._cout.wait_event(ev_done[i])
                     self.out_host[tok[i]:tok[i + 1]].copy_(self.out_d[tok[i]:tok[i + 1]], non_blocking=True)
             main.wait_stream(self._cin)

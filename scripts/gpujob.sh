@@ -80,6 +80,7 @@ for r in "$@"; do
                env $v timeout 300 python scripts/perf.py time --tag "[$v]" --shapes C2,C4shard,C2fp8,d64x512,d1x8k,d16x512,C2kv2,C4kv1
              done > ${O}_mergeab.log 2>&1; cat ${O}_mergeab.log ;;
     e2e) timeout 600 python scripts/perf.py e2e > ${O}_e2e.log 2>&1; cat ${O}_e2e.log ;;
+    pfe2e) timeout 900 python scripts/perf.py pfe2e > ${O}_pfe2e.log 2>&1; cat ${O}_pfe2e.log ;;
     bandab) for b in 0 16 8 32; do B200ATTN_PREFILL_BAND=$b timeout 600 python scripts/perf.py time --op prefill \
               --shapes C3,1x16k,4x8k,16x8k,1x32k,16x2k --tag band$b; done > ${O}_bandab.log 2>&1; cat ${O}_bandab.log ;;
     bandtests) timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "banded or c3_full or every_compiled" \

@@ -334,9 +334,57 @@ def cmd_e2e(a):
     print(json.dumps({"tag": a.tag, **{k: round(v, 2) for k, v in res.items()}}), flush=True)
 
 
+def cmd_pfe2e(a):
+    """Where the prefill e2e step's time goes (C3): the PCIe copies alone (H2D of q/k/v, D2H of the
+    output, and both directions at once) against attention.PrefillStep at several group counts."""
+    x = W.make_prefill(W.C3, device="cpu")
+    st = torch.cuda.current_stream()
+
+    def ev_time(fn, n=5):
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(st)
+        for _ in range(n):
+            fn()
+        e.record(st)
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / n
+
+    res = {}
+    nin = (x.q.numel() + x.k.numel() + x.v.numel()) * 2
+    nout = x.q.numel() * 2
+    hi = torch.empty(nin, dtype=torch.uint8).pin_memory()
+    di = torch.empty(nin, dtype=torch.uint8, device="cuda")
+    ho = torch.empty(nout, dtype=torch.uint8).pin_memory()
+    do = torch.empty(nout, dtype=torch.uint8, device="cuda")
+    res["h2d_ms"] = ev_time(lambda: di.copy_(hi, non_blocking=True))
+    res["d2h_ms"] = ev_time(lambda: ho.copy_(do, non_blocking=True))
+    s2 = torch.cuda.Stream()
+
+    def both():
+        s2.wait_stream(st)
+        with torch.cuda.stream(s2):
+            ho.copy_(do, non_blocking=True)
+        di.copy_(hi, non_blocking=True)
+        st.wait_stream(s2)
+    res["both_ms"] = ev_time(both)
+    res["h2d_GBps"] = nin / res["h2d_ms"] / 1e6
+    res["d2h_GBps"] = nout / res["d2h_ms"] / 1e6
+    del hi, di, ho, do
+    for chunks in (2, 4, 8, 16):
+        step = A.PrefillStep(x.lens, x.q.shape[1], x.k.shape[1], x.q.shape[2], chunks=chunks)
+        step.set_inputs(x.q, x.k, x.v)
+        res[f"step_chunks{chunks}_ms"] = ev_time(step)
+        del step
+        torch.cuda.empty_cache()
+    print(json.dumps({"tag": a.tag, **{k: round(v, 3) for k, v in res.items()}}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("cmd", choices=["time", "single", "prof", "trace", "umma-rate", "e2e", "dtrace", "c1trace", "ptrace"])
+    ap.add_argument("cmd", choices=["time", "single", "prof", "trace", "umma-rate", "e2e", "dtrace", "c1trace", "ptrace",
+                                    "pfe2e"])
     ap.add_argument("args", nargs="*")
     ap.add_argument("--op", default="prefill")
     ap.add_argument("--shapes", default="C3")
@@ -348,7 +396,7 @@ def main():
     ap.add_argument("--tag", default="")
     ap.add_argument("--per-cta", action="store_true", help="dtrace: per-CTA sm id / first S / last P")
     a = ap.parse_args()
-    {"time": cmd_time, "single": cmd_single, "prof": cmd_prof, "trace": cmd_trace, "umma-rate": cmd_umma_rate, "e2e": cmd_e2e, "dtrace": cmd_dtrace,
+    {"time": cmd_time, "single": cmd_single, "prof": cmd_prof, "trace": cmd_trace, "umma-rate": cmd_umma_rate, "e2e": cmd_e2e, "pfe2e": cmd_pfe2e, "dtrace": cmd_dtrace,
      "c1trace": cmd_c1trace, "ptrace": cmd_ptrace}[a.cmd](a)
 
 
